@@ -1,0 +1,189 @@
+/*
+ * cake_cuda.h — thin C-ABI CUDA layer underneath the cake:: host runtime.
+ *
+ * This is the "L3.5" layer of SURVEY.md §1: the reference (C++20, host
+ * threads only) has no device code at all — its compute side sleeps for a
+ * modeled latency (reference proj/src/compute.cpp:48-49) and its loader lands
+ * bytes in heap buffers (proj/src/transfer.cpp:149-170). Every entry point
+ * here is what the B200 build puts in place of one of those stand-ins:
+ *
+ *   cake_prefill_chunk      replaces sleep_for_us(compute_latency(...))
+ *                           in ComputeEngine::run_forward (compute.cpp:48-49)
+ *   cake_kv_scatter         replaces the heap landing of TransferEngine's
+ *                           reader/pacer (transfer.cpp:149-170, 209-225) with
+ *                           a staging -> paged-KV permutation on the copy stream
+ *   cake_event_*            replace ResidentSet's mutex hand-off
+ *                           (transfer.cpp:9-24): residency = event completed
+ *   cake_final_logits       first-token step the reference never models
+ *                           (its TTFT stops at KV residency, report.hpp:39)
+ *
+ * Conventions: plain C types only; every call returns int status
+ * (0 = ok, > 0 = the cudaError_t / ncclResult_t that failed offset by
+ * CAKE_ECUDA / CAKE_ENCCL, < 0 = cake validation errors); a message for the
+ * last failure on the calling thread is available from cake_cuda_last_error.
+ * Streams and events are opaque void* handles. All launches are
+ * stream-ordered; nothing blocks except *_sync calls.
+ */
+#ifndef CAKE_CUDA_H_
+#define CAKE_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CAKE_API __attribute__((visibility("default")))
+#else
+#define CAKE_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  CAKE_OK = 0,
+  CAKE_EINVAL = -1,
+  CAKE_ENOMEM = -2,
+  CAKE_ESTATE = -3,
+  CAKE_ENOTREADY = 1, /* cake_event_query: work still pending */
+  CAKE_ECUDA = 1000,  /* + cudaError_t */
+  CAKE_ENCCL = 2000   /* + ncclResult_t */
+};
+
+CAKE_API int cake_cuda_last_error(char* buf, size_t len);
+CAKE_API int cake_cuda_version(int* runtime, int* driver);
+CAKE_API int cake_cuda_device_count(int* n);
+CAKE_API int cake_cuda_set_device(int device);
+CAKE_API int cake_cuda_sm_count(int device, int* n);
+CAKE_API int cake_cuda_device_sync(void);
+
+/* ---------------------------------------------------------- streams/events */
+CAKE_API int cake_stream_create(void** stream, int high_priority);
+CAKE_API int cake_stream_destroy(void* stream);
+CAKE_API int cake_stream_sync(void* stream);
+CAKE_API int cake_stream_wait_event(void* stream, void* event);
+CAKE_API int cake_event_create(void** event, int timing);
+CAKE_API int cake_event_destroy(void* event);
+CAKE_API int cake_event_record(void* event, void* stream);
+CAKE_API int cake_event_query(void* event); /* CAKE_OK when complete, CAKE_ENOTREADY if pending */
+CAKE_API int cake_event_sync(void* event);
+CAKE_API int cake_event_elapsed_ms(void* start, void* stop, float* ms);
+
+/* ---------------------------------------------------------- memory */
+CAKE_API int cake_host_alloc(void** p, size_t bytes);  /* pinned, portable */
+CAKE_API int cake_host_free(void* p);
+CAKE_API int cake_host_register(void* p, size_t bytes);
+CAKE_API int cake_host_unregister(void* p);
+CAKE_API int cake_dev_alloc(void** p, size_t bytes);
+CAKE_API int cake_dev_free(void* p);
+CAKE_API int cake_memset_async(void* dst, int value, size_t bytes, void* stream);
+CAKE_API int cake_h2d_async(void* dst, const void* src, size_t bytes, void* stream);
+CAKE_API int cake_d2h_async(void* dst, const void* src, size_t bytes, void* stream);
+CAKE_API int cake_d2d_async(void* dst, const void* src, size_t bytes, void* stream);
+
+/* ---------------------------------------------------------- model */
+typedef struct cake_model_config {
+  int n_layers;
+  int hidden;
+  int n_heads;     /* query heads, whole model */
+  int n_kv_heads;  /* KV heads, whole model */
+  int head_dim;    /* 64 or 128 */
+  int ffn;         /* MLP intermediate size, whole model */
+  int vocab;
+  float rope_theta;
+  float rms_eps;
+  int page_tokens; /* KV page size; 64 */
+  int max_chunk;   /* largest chunk (rows) the activation scratch holds */
+  long long max_tokens; /* KV capacity (logical pages = ceil(max_tokens / page_tokens)) */
+  int spare_pages; /* extra physical pages (second page set of a contested chunk) */
+  int tp_rank;
+  int tp_size;
+  unsigned long long seed;
+} cake_model_config;
+
+typedef struct cake_model_info {
+  long long kv_bytes_per_token;   /* this rank's shard */
+  long long page_bytes;           /* one physical page, all layers */
+  int n_logical_pages;
+  int n_physical_pages;
+  int local_q_heads, local_kv_heads, local_ffn;
+  long long weight_bytes;
+  long long flops_per_token_linear; /* 2 * (this rank's projection weights), no LM head */
+  void* kv_pool;
+} cake_model_info;
+
+typedef struct cake_model cake_model;
+
+CAKE_API int cake_model_create(const cake_model_config* cfg, cake_model** out);
+CAKE_API int cake_model_destroy(cake_model* m);
+CAKE_API int cake_model_get_info(const cake_model* m, cake_model_info* out);
+/* Attach an NCCL communicator (ncclComm_t) for tp_size > 1. */
+CAKE_API int cake_model_set_comm(cake_model* m, void* nccl_comm);
+
+enum {
+  CAKE_PREFILL_NO_KV_WRITE = 1 /* q-only pass (first-token step over a complete cache) */
+};
+
+/* One chunk of prefill through every layer on `stream`. d_tokens: the
+ * chunk's chunk_len token ids (device int32). d_block_table: logical page ->
+ * physical page. d_abort (optional): device int; when non-zero at a kernel's
+ * start the kernel exits (lost race / cancelled chunk). */
+CAKE_API int cake_prefill_chunk(cake_model* m, const int32_t* d_tokens, long long chunk_start, int chunk_len,
+                       const int32_t* d_block_table, const int32_t* d_abort, int flags, void* stream);
+
+/* First-token logits (fp32 [vocab]) of a prompt of T tokens whose KV is fully
+ * resident. recompute = 1: run the last token as a 1-row q-only pass over the
+ * cache (needed when the tail chunk was loaded, not computed); recompute = 0:
+ * use row `last_row` of the hidden state the last prefill_chunk left behind. */
+CAKE_API int cake_final_logits(cake_model* m, long long T, const int32_t* d_last_token, int recompute,
+                      int last_row, const int32_t* d_block_table, float* d_logits, void* stream);
+
+/* ---------------------------------------------------------- KV loader */
+/* Bytes of one chunk of chunk_len tokens in the cache-tier format
+ * [layer][K|V][kv_head][token][head_dim] bf16 (this rank's shard). */
+CAKE_API long long cake_kv_chunk_bytes(const cake_model* m, int chunk_len);
+/* staging bytes [byte_begin, byte_end) (16-B aligned) of a chunk starting at
+ * token chunk_start -> paged pool through d_block_table. */
+CAKE_API int cake_kv_scatter(cake_model* m, const void* d_staging, long long chunk_start, int chunk_len,
+                    const int32_t* d_block_table, long long byte_begin, long long byte_end,
+                    void* stream);
+/* Inverse: paged pool -> staging (cache-tier format). */
+CAKE_API int cake_kv_gather(cake_model* m, void* d_staging, long long chunk_start, int chunk_len,
+                   const int32_t* d_block_table, void* stream);
+
+/* ---------------------------------------------------------- profiling */
+enum {
+  CAKE_K_EMBED = 0,
+  CAKE_K_RMSNORM,
+  CAKE_K_GEMM_QKV,
+  CAKE_K_ATTN,
+  CAKE_K_GEMM_O,
+  CAKE_K_GEMM_GU,
+  CAKE_K_GEMM_D,
+  CAKE_K_ALLREDUCE,
+  CAKE_K_LMHEAD,
+  CAKE_K_SCATTER,
+  CAKE_K_COUNT
+};
+typedef struct cake_kernel_stat {
+  long long launches;
+  double total_ms;
+  double flops;  /* algorithmic */
+  double bytes;  /* algorithmic */
+} cake_kernel_stat;
+/* When enabled, every launch of a tracked kernel class is bracketed by CUDA
+ * events on its stream; stats resolve (and reset) on read. */
+CAKE_API int cake_model_set_profiling(cake_model* m, int enabled);
+CAKE_API int cake_model_kernel_stats(cake_model* m, cake_kernel_stat* out /* [CAKE_K_COUNT] */, int reset);
+CAKE_API int cake_model_launch_count(cake_model* m, long long* n, int reset);
+
+/* ---------------------------------------------------------- unit entry points */
+/* C = A · B^T for bf16 row-major A [M, K], B [N, K]; epi 0: bf16 C, 1: fp32 C,
+ * 2: fp32 C += . block_n 128 or 256. For tests and microbenchmarks. */
+CAKE_API int cake_gemm(const void* dA, const void* dB, void* dC, int M, int N, int K, int epi, int block_n,
+              void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CAKE_CUDA_H_ */

@@ -1,0 +1,879 @@
+// Host side of the C-ABI CUDA layer (include/cake_cuda.h): device memory,
+// streams/events, the Llama-shaped model (seeded weights, paged KV pool,
+// activation scratch, TMA descriptors) and the launch sequence of one chunk.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "attention.cuh"
+#include "cake_cuda.h"
+#include "elementwise.cuh"
+#include "gemm.cuh"
+
+using namespace cake_dev;
+using bf16 = __nv_bfloat16;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CK(expr)                                                                           \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(CAKE_ECUDA + static_cast<int>(e_), "%s: %s (%s:%d)", #expr,             \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                             \
+  } while (0)
+
+#define CKL()                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = cudaGetLastError();                                                   \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(CAKE_ECUDA + static_cast<int>(e_), "launch: %s (%s:%d)",                 \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                             \
+  } while (0)
+
+#define CKS(expr)                                                                          \
+  do {                                                                                     \
+    int s_ = (expr);                                                                       \
+    if (s_ != CAKE_OK) return s_;                                                          \
+  } while (0)
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------ TMA maps
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// Row-major bf16 [rows, cols] with a (64 x box_rows) SW128 box.
+int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(CAKE_ESTATE, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t elem[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                  elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CAKE_EINVAL, "tensor map encode failed (%d) rows=%llu cols=%llu", (int)r,
+                                     (unsigned long long)rows, (unsigned long long)cols);
+  return CAKE_OK;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <int BN, int EPI>
+int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaStream_t s) {
+  using Cfg = GemmCfg<BN>;
+  auto kern = gemm_tc_kernel<BN, EPI>;
+  static bool configured = false;
+  if (!configured) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+    configured = true;
+  }
+  a.num_m_blocks = (a.M + kGemmBlockM - 1) / kGemmBlockM;
+  a.num_n_blocks = a.N / BN;
+  a.num_k_blocks = a.K / kGemmBlockK;
+  const int tiles = a.num_m_blocks * a.num_n_blocks;
+  const int grid = std::min(tiles, num_sms());
+  kern<<<grid, kGemmThreads, Cfg::kSmemBytes, s>>>(ta, tb, a);
+  CKL();
+  return CAKE_OK;
+}
+
+int gemm_dispatch(int bn, int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+                  cudaStream_t s) {
+  if (bn == 256) {
+    switch (epi) {
+      case kEpiBf16: return launch_gemm<256, kEpiBf16>(ta, tb, a, s);
+      case kEpiF32: return launch_gemm<256, kEpiF32>(ta, tb, a, s);
+      case kEpiResid: return launch_gemm<256, kEpiResid>(ta, tb, a, s);
+      case kEpiSwiglu: return launch_gemm<256, kEpiSwiglu>(ta, tb, a, s);
+      case kEpiQkv: return launch_gemm<256, kEpiQkv>(ta, tb, a, s);
+    }
+  } else if (bn == 128) {
+    switch (epi) {
+      case kEpiBf16: return launch_gemm<128, kEpiBf16>(ta, tb, a, s);
+      case kEpiF32: return launch_gemm<128, kEpiF32>(ta, tb, a, s);
+      case kEpiResid: return launch_gemm<128, kEpiResid>(ta, tb, a, s);
+      case kEpiQkv: return launch_gemm<128, kEpiQkv>(ta, tb, a, s);
+    }
+  }
+  return fail(CAKE_EINVAL, "gemm: unsupported block_n=%d epi=%d", bn, epi);
+}
+
+int launch_grid_for(long long work, int threads) {
+  long long blocks = (work + threads - 1) / threads;
+  long long cap = static_cast<long long>(num_sms()) * 8;
+  return static_cast<int>(std::max<long long>(1, std::min(blocks, cap)));
+}
+
+}  // namespace
+
+// ====================================================================== model
+struct LayerWeights {
+  bf16* wqkv = nullptr;  // [(nq + 2 nkv) * hd, H]   local heads
+  bf16* wo = nullptr;    // [H, nq * hd]             local input columns
+  bf16* wgu = nullptr;   // [2 * F, H]               gate|up interleaved per 128 rows
+  bf16* wd = nullptr;    // [H, F]                   local input columns
+  bf16* ln1 = nullptr;
+  bf16* ln2 = nullptr;
+  CUtensorMap m_qkv, m_o, m_gu, m_d;
+};
+
+struct ProfPair {
+  int kind;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+
+struct cake_model {
+  cake_model_config cfg{};
+  int nq = 0, nkv = 0, F = 0, hd = 0, H = 0, L = 0;
+  int qkv_rows = 0;
+  int bn_qkv = 256;
+  std::vector<LayerWeights> layers;
+  void* weight_arena = nullptr;
+  size_t weight_bytes = 0;
+  bf16* embed = nullptr;
+  bf16* final_norm = nullptr;
+  bf16* lm_head = nullptr;
+  bf16* pool = nullptr;
+  size_t pool_bytes = 0;
+  int n_logical_pages = 0, n_phys_pages = 0;
+  float2* rope = nullptr;
+  int rows_cap = 0;  // scratch rows (multiple of 128)
+  float* h = nullptr;
+  bf16* xn = nullptr;
+  bf16* q = nullptr;
+  bf16* attn = nullptr;
+  bf16* act = nullptr;
+  float* part_o = nullptr;
+  float* part_lse = nullptr;
+  int max_splits = 16;
+  size_t part_rows_cap = 0;  // splits * chunk rows * local q heads the partials hold
+  float* tp_buf = nullptr;  // fp32 partial sums for the TP all-reduce
+  CUtensorMap a_xn, a_attn, a_act;
+  ncclComm_t comm = nullptr;
+  bool profiling = false;
+  std::vector<ProfPair> prof;
+  std::vector<cudaEvent_t> event_pool;
+  cake_kernel_stat stats[CAKE_K_COUNT]{};
+  long long launches = 0;
+};
+
+namespace {
+
+cudaEvent_t pool_event(cake_model* m) {
+  if (!m->event_pool.empty()) {
+    cudaEvent_t e = m->event_pool.back();
+    m->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets a launch with events when profiling is on.
+struct ProfScope {
+  cake_model* m;
+  int kind;
+  cudaStream_t s;
+  double flops, bytes;
+  cudaEvent_t a = nullptr;
+  ProfScope(cake_model* m_, int kind_, cudaStream_t s_, double f, double b)
+      : m(m_), kind(kind_), s(s_), flops(f), bytes(b) {
+    m->launches++;
+    if (m->profiling) {
+      a = pool_event(m);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~ProfScope() {
+    if (m->profiling) {
+      cudaEvent_t b = pool_event(m);
+      cudaEventRecord(b, s);
+      m->prof.push_back({kind, a, b, flops, bytes});
+    }
+  }
+};
+
+int alloc_dev(void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  CK(cudaMalloc(p, bytes));
+  return CAKE_OK;
+}
+
+int init_tensor(bf16* dst, long long rows, long long cols, long long row_off, long long col_off,
+                long long logical_cols, long long group, long long group_stride, uint64_t seed,
+                uint32_t tid, float scale, cudaStream_t s) {
+  InitArgs a;
+  a.dst = dst;
+  a.rows = rows;
+  a.cols = cols;
+  a.dst_ld = cols;
+  a.row_off = row_off;
+  a.col_off = col_off;
+  a.logical_cols = logical_cols;
+  a.group = group;
+  a.group_stride = group_stride;
+  a.seed = seed;
+  a.tensor_id = tid;
+  a.scale = scale;
+  init_weight_kernel<<<launch_grid_for(rows * cols, 256), 256, 0, s>>>(a);
+  CKL();
+  return CAKE_OK;
+}
+
+int fill(bf16* dst, long long n, float v, cudaStream_t s) {
+  fill_bf16_kernel<<<launch_grid_for(n, 256), 256, 0, s>>>(dst, n, v);
+  CKL();
+  return CAKE_OK;
+}
+
+// Tensor ids of the seeded generator (shared with oracle/llama_ref.c).
+uint32_t tid_layer(int layer, int which) { return static_cast<uint32_t>(16 * layer + which); }
+constexpr uint32_t kTidEmbed = 1u << 20;
+constexpr uint32_t kTidLmHead = (1u << 20) + 1;
+enum { kWq = 0, kWk = 1, kWv = 2, kWo = 3, kWgate = 4, kWup = 5, kWdown = 6 };
+
+}  // namespace
+
+namespace {
+
+int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, const int32_t* bt,
+              const int32_t* abort_flag, cudaStream_t s) {
+  const int G = m->nq / m->nkv;
+  const int tok_per_tile = kAttnRows / G;
+  const int qtiles = (chunk_len + tok_per_tile - 1) / tok_per_tile;
+  const long long kv_end = chunk_start + chunk_len;
+  const int n_pages = static_cast<int>((kv_end + kAttnPage - 1) / kAttnPage);
+  const int base_ctas = qtiles * m->nkv;
+  const int target = 2 * num_sms();
+  const int cap = static_cast<int>(m->part_rows_cap / (static_cast<size_t>(chunk_len) * m->nq));
+  int splits = std::max(1, std::min({(target + base_ctas - 1) / base_ctas, std::max(1, n_pages / 4), m->max_splits, cap}));
+  AttnArgs a;
+  a.q = m->q;
+  a.pool = m->pool;
+  a.block_table = bt;
+  a.out = m->attn;
+  a.part_o = m->part_o;
+  a.part_lse = m->part_lse;
+  a.chunk_start = chunk_start;
+  a.chunk_len = chunk_len;
+  a.n_q_heads = m->nq;
+  a.n_kv_heads = m->nkv;
+  a.layer = layer;
+  a.n_layers = m->L;
+  a.num_splits = splits;
+  a.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(m->hd));
+  a.abort_flag = abort_flag;
+  // algorithmic work: 4 * hd * (visible keys) per (query, head)
+  const double vis = static_cast<double>(chunk_len) * chunk_start + 0.5 * chunk_len * (chunk_len + 1.0);
+  const double flops = 4.0 * m->hd * m->nq * vis;
+  const double bytes = static_cast<double>(kv_end) * m->nkv * m->hd * 2 * 2 + 2.0 * chunk_len * m->nq * m->hd * 2;
+  ProfScope ps(m, CAKE_K_ATTN, s, flops, bytes);
+  dim3 grid(qtiles, m->nkv, splits);
+  const int smem = (kAttnRows + 4 * kAttnPage) * m->hd * 2;
+  if (m->hd == 128) {
+    static bool cfgd = false;
+    if (!cfgd) {
+      CK(cudaFuncSetAttribute(attn_prefill_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      cfgd = true;
+    }
+    attn_prefill_kernel<128><<<grid, kAttnThreads, smem, s>>>(a);
+  } else {
+    static bool cfgd = false;
+    if (!cfgd) {
+      CK(cudaFuncSetAttribute(attn_prefill_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      cfgd = true;
+    }
+    attn_prefill_kernel<64><<<grid, kAttnThreads, smem, s>>>(a);
+  }
+  CKL();
+  if (splits > 1) {
+    const int rows = chunk_len * m->nq;
+    const int wpb = 8;
+    if (m->hd == 128)
+      attn_combine_kernel<128><<<(rows + wpb - 1) / wpb, wpb * 32, 0, s>>>(m->part_o, m->part_lse, m->attn, rows, splits,
+                                                                          abort_flag);
+    else
+      attn_combine_kernel<64><<<(rows + wpb - 1) / wpb, wpb * 32, 0, s>>>(m->part_o, m->part_lse, m->attn, rows, splits,
+                                                                         abort_flag);
+    CKL();
+  }
+  return CAKE_OK;
+}
+
+int rmsnorm(cake_model* m, const bf16* gamma, long long row0, int rows, const int32_t* abort_flag, cudaStream_t s) {
+  ProfScope ps(m, CAKE_K_RMSNORM, s, 0.0, static_cast<double>(rows) * m->H * 6);
+  rmsnorm_kernel<<<rows, 256, 0, s>>>(m->h, gamma, m->xn, m->H, m->cfg.rms_eps, row0, abort_flag);
+  CKL();
+  return CAKE_OK;
+}
+
+// Row-parallel projection output: residual += acc (TP: via all-reduce of partials).
+int row_parallel(cake_model* m, int kind, const CUtensorMap& ta, const CUtensorMap& tb, int K, int M,
+                 const int32_t* abort_flag, cudaStream_t s) {
+  GemmArgs g{};
+  g.M = M;
+  g.N = m->H;
+  g.K = K;
+  g.abort_flag = abort_flag;
+  const double flops = 2.0 * M * m->H * K;
+  const double bytes = 2.0 * m->H * K + 2.0 * M * K + 8.0 * M * m->H;
+  if (m->cfg.tp_size == 1) {
+    g.resid = m->h;
+    g.ldr = m->H;
+    ProfScope ps(m, kind, s, flops, bytes);
+    return gemm_dispatch(128, kEpiResid, ta, tb, g, s);
+  }
+  if (!m->comm) return fail(CAKE_ESTATE, "tp_size > 1 but no NCCL communicator attached");
+  g.out = m->tp_buf;
+  g.ldo = m->H;
+  {
+    ProfScope ps(m, kind, s, flops, bytes);
+    CKS(gemm_dispatch(128, kEpiF32, ta, tb, g, s));
+  }
+  {
+    ProfScope ps(m, CAKE_K_ALLREDUCE, s, 0.0, 4.0 * M * m->H);
+    ncclResult_t r = ncclAllReduce(m->tp_buf, m->tp_buf, static_cast<size_t>(M) * m->H, ncclFloat32, ncclSum,
+                                   m->comm, s);
+    if (r != ncclSuccess) return fail(CAKE_ENCCL + r, "allreduce: %s", ncclGetErrorString(r));
+  }
+  add_inplace_kernel<<<launch_grid_for(static_cast<long long>(M) * m->H / 4, 256), 256, 0, s>>>(
+      m->h, m->tp_buf, static_cast<long long>(M) * m->H, abort_flag);
+  CKL();
+  return CAKE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cake_cuda_last_error(char* buf, size_t len) {
+  if (buf && len) {
+    std::snprintf(buf, len, "%s", g_last_error.c_str());
+  }
+  return static_cast<int>(g_last_error.size());
+}
+
+int cake_cuda_version(int* runtime, int* driver) {
+  CK(cudaRuntimeGetVersion(runtime));
+  CK(cudaDriverGetVersion(driver));
+  return CAKE_OK;
+}
+
+int cake_cuda_device_count(int* n) {
+  cudaError_t e = cudaGetDeviceCount(n);
+  if (e != cudaSuccess) {
+    *n = 0;
+    cudaGetLastError();
+  }
+  return CAKE_OK;
+}
+
+int cake_cuda_set_device(int device) {
+  CK(cudaSetDevice(device));
+  g_num_sms = 0;
+  return CAKE_OK;
+}
+
+int cake_cuda_sm_count(int device, int* n) {
+  CK(cudaDeviceGetAttribute(n, cudaDevAttrMultiProcessorCount, device));
+  return CAKE_OK;
+}
+
+int cake_cuda_device_sync(void) {
+  CK(cudaDeviceSynchronize());
+  return CAKE_OK;
+}
+
+int cake_stream_create(void** stream, int high_priority) {
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  cudaStream_t s;
+  CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, high_priority ? hi : lo));
+  *stream = s;
+  return CAKE_OK;
+}
+int cake_stream_destroy(void* stream) {
+  CK(cudaStreamDestroy(S(stream)));
+  return CAKE_OK;
+}
+int cake_stream_sync(void* stream) {
+  CK(cudaStreamSynchronize(S(stream)));
+  return CAKE_OK;
+}
+int cake_stream_wait_event(void* stream, void* event) {
+  CK(cudaStreamWaitEvent(S(stream), static_cast<cudaEvent_t>(event), 0));
+  return CAKE_OK;
+}
+int cake_event_create(void** event, int timing) {
+  cudaEvent_t e;
+  CK(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+  *event = e;
+  return CAKE_OK;
+}
+int cake_event_destroy(void* event) {
+  CK(cudaEventDestroy(static_cast<cudaEvent_t>(event)));
+  return CAKE_OK;
+}
+int cake_event_record(void* event, void* stream) {
+  CK(cudaEventRecord(static_cast<cudaEvent_t>(event), S(stream)));
+  return CAKE_OK;
+}
+int cake_event_query(void* event) {
+  cudaError_t e = cudaEventQuery(static_cast<cudaEvent_t>(event));
+  if (e == cudaSuccess) return CAKE_OK;
+  if (e == cudaErrorNotReady) return CAKE_ENOTREADY;
+  return fail(CAKE_ECUDA + static_cast<int>(e), "event query: %s", cudaGetErrorString(e));
+}
+int cake_event_sync(void* event) {
+  CK(cudaEventSynchronize(static_cast<cudaEvent_t>(event)));
+  return CAKE_OK;
+}
+int cake_event_elapsed_ms(void* start, void* stop, float* ms) {
+  CK(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(start), static_cast<cudaEvent_t>(stop)));
+  return CAKE_OK;
+}
+
+int cake_host_alloc(void** p, size_t bytes) {
+  CK(cudaHostAlloc(p, bytes ? bytes : 16, cudaHostAllocPortable));
+  return CAKE_OK;
+}
+int cake_host_free(void* p) {
+  CK(cudaFreeHost(p));
+  return CAKE_OK;
+}
+int cake_host_register(void* p, size_t bytes) {
+  CK(cudaHostRegister(p, bytes, cudaHostRegisterPortable));
+  return CAKE_OK;
+}
+int cake_host_unregister(void* p) {
+  CK(cudaHostUnregister(p));
+  return CAKE_OK;
+}
+int cake_dev_alloc(void** p, size_t bytes) { return alloc_dev(p, bytes); }
+int cake_dev_free(void* p) {
+  CK(cudaFree(p));
+  return CAKE_OK;
+}
+int cake_memset_async(void* dst, int value, size_t bytes, void* stream) {
+  CK(cudaMemsetAsync(dst, value, bytes, S(stream)));
+  return CAKE_OK;
+}
+int cake_h2d_async(void* dst, const void* src, size_t bytes, void* stream) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, S(stream)));
+  return CAKE_OK;
+}
+int cake_d2h_async(void* dst, const void* src, size_t bytes, void* stream) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, S(stream)));
+  return CAKE_OK;
+}
+int cake_d2d_async(void* dst, const void* src, size_t bytes, void* stream) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, S(stream)));
+  return CAKE_OK;
+}
+
+// ---------------------------------------------------------------- model
+int cake_model_destroy(cake_model* m) {
+  if (!m) return CAKE_OK;
+  cudaDeviceSynchronize();
+  for (void* p : {static_cast<void*>(m->weight_arena), static_cast<void*>(m->pool),
+                  static_cast<void*>(m->rope), static_cast<void*>(m->h), static_cast<void*>(m->xn),
+                  static_cast<void*>(m->q), static_cast<void*>(m->attn), static_cast<void*>(m->act),
+                  static_cast<void*>(m->part_o), static_cast<void*>(m->part_lse),
+                  static_cast<void*>(m->tp_buf)})
+    if (p) cudaFree(p);
+  for (auto& p : m->prof) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : m->event_pool) cudaEventDestroy(e);
+  delete m;
+  return CAKE_OK;
+}
+
+int cake_model_create(const cake_model_config* cfg, cake_model** out) {
+  *out = nullptr;
+  const cake_model_config& c = *cfg;
+  if (c.n_layers < 1 || c.hidden < 64 || c.n_heads < 1 || c.n_kv_heads < 1 || c.vocab < 1)
+    return fail(CAKE_EINVAL, "model: bad dimensions");
+  if (c.head_dim != 64 && c.head_dim != 128) return fail(CAKE_EINVAL, "model: head_dim must be 64 or 128");
+  if (c.page_tokens != kAttnPage) return fail(CAKE_EINVAL, "model: page_tokens must be %d", kAttnPage);
+  if (c.tp_size < 1 || c.tp_rank < 0 || c.tp_rank >= c.tp_size) return fail(CAKE_EINVAL, "model: bad tp");
+  if (c.n_heads % c.n_kv_heads || c.n_kv_heads % c.tp_size || c.n_heads % c.tp_size)
+    return fail(CAKE_EINVAL, "model: heads must divide evenly (GQA groups, TP shards)");
+  if (c.ffn % (128 * c.tp_size)) return fail(CAKE_EINVAL, "model: ffn / tp must be a multiple of 128");
+  if (c.hidden % 128) return fail(CAKE_EINVAL, "model: hidden must be a multiple of 128");
+  if (c.max_chunk < 1 || c.max_tokens < 1) return fail(CAKE_EINVAL, "model: bad capacity");
+  const int G = c.n_heads / c.n_kv_heads;
+  if (kAttnRows % G) return fail(CAKE_EINVAL, "model: GQA group must divide %d", kAttnRows);
+
+  auto* m = new cake_model();
+  m->cfg = c;
+  m->L = c.n_layers;
+  m->H = c.hidden;
+  m->hd = c.head_dim;
+  m->nq = c.n_heads / c.tp_size;
+  m->nkv = c.n_kv_heads / c.tp_size;
+  m->F = c.ffn / c.tp_size;
+  m->qkv_rows = (m->nq + 2 * m->nkv) * m->hd;
+  m->bn_qkv = (m->qkv_rows % 256 == 0) ? 256 : 128;
+  if (m->qkv_rows % m->bn_qkv) {
+    delete m;
+    return fail(CAKE_EINVAL, "model: qkv rows %d not tileable", m->qkv_rows);
+  }
+  cudaStream_t s = 0;
+  int st = CAKE_OK;
+  auto bail = [&](int code) {
+    cake_model_destroy(m);
+    return code;
+  };
+
+  // ---- weights (one arena, every tensor 128-B aligned)
+  const size_t H = m->H, F = m->F, hd = m->hd, V = c.vocab;
+  auto pad = [](size_t n) { return (n + 63) / 64 * 64; };
+  const size_t per_layer =
+      pad(m->qkv_rows * H) + pad(H * m->nq * hd) + pad(2 * F * H) + pad(H * F) + 2 * pad(H);
+  m->weight_bytes = (per_layer * m->L + 2 * pad(V * H) + pad(H)) * sizeof(bf16);
+  if ((st = alloc_dev(&m->weight_arena, m->weight_bytes))) return bail(st);
+  bf16* w = static_cast<bf16*>(m->weight_arena);
+  auto take = [&](size_t n) {
+    bf16* p = w;
+    w += pad(n);
+    return p;
+  };
+  const uint64_t seed = c.seed;
+  const int r = c.tp_rank;
+  const float s_h = 1.0f / std::sqrt(static_cast<float>(c.hidden));
+  const float s_o = 1.0f / std::sqrt(static_cast<float>(c.n_heads * c.head_dim));
+  const float s_f = 1.0f / std::sqrt(static_cast<float>(c.ffn));
+  m->layers.resize(m->L);
+  for (int l = 0; l < m->L; ++l) {
+    LayerWeights& lw = m->layers[l];
+    lw.wqkv = take(m->qkv_rows * H);
+    lw.wo = take(H * m->nq * hd);
+    lw.wgu = take(2 * F * H);
+    lw.wd = take(H * F);
+    lw.ln1 = take(H);
+    lw.ln2 = take(H);
+    const long long qrows = static_cast<long long>(m->nq) * hd, kvrows = static_cast<long long>(m->nkv) * hd;
+    if ((st = init_tensor(lw.wqkv, qrows, H, r * qrows, 0, H, 0, 0, seed, tid_layer(l, kWq), s_h, s))) return bail(st);
+    if ((st = init_tensor(lw.wqkv + qrows * H, kvrows, H, r * kvrows, 0, H, 0, 0, seed, tid_layer(l, kWk), s_h, s)))
+      return bail(st);
+    if ((st = init_tensor(lw.wqkv + (qrows + kvrows) * H, kvrows, H, r * kvrows, 0, H, 0, 0, seed,
+                          tid_layer(l, kWv), s_h, s)))
+      return bail(st);
+    if ((st = init_tensor(lw.wo, H, m->nq * hd, 0, r * qrows, c.n_heads * hd, 0, 0, seed, tid_layer(l, kWo), s_o, s)))
+      return bail(st);
+    // gate|up interleave: physical 256-row block b = [gate rows b*128..+128 | up rows b*128..+128]
+    for (long long b = 0; b < static_cast<long long>(F) / 128; ++b) {
+      if ((st = init_tensor(lw.wgu + (2 * b) * 128 * H, 128, H, r * F + b * 128, 0, H, 0, 0, seed,
+                            tid_layer(l, kWgate), s_h, s)))
+        return bail(st);
+      if ((st = init_tensor(lw.wgu + (2 * b + 1) * 128 * H, 128, H, r * F + b * 128, 0, H, 0, 0, seed,
+                            tid_layer(l, kWup), s_h, s)))
+        return bail(st);
+    }
+    if ((st = init_tensor(lw.wd, H, F, 0, r * F, c.ffn, 0, 0, seed, tid_layer(l, kWdown), s_f, s))) return bail(st);
+    if ((st = fill(lw.ln1, H, 1.0f, s))) return bail(st);
+    if ((st = fill(lw.ln2, H, 1.0f, s))) return bail(st);
+    if ((st = make_map(&lw.m_qkv, lw.wqkv, m->qkv_rows, H, m->bn_qkv))) return bail(st);
+    if ((st = make_map(&lw.m_o, lw.wo, H, m->nq * hd, 128))) return bail(st);
+    if ((st = make_map(&lw.m_gu, lw.wgu, 2 * F, H, 256))) return bail(st);
+    if ((st = make_map(&lw.m_d, lw.wd, H, F, 128))) return bail(st);
+  }
+  m->embed = take(V * H);
+  m->lm_head = take(V * H);
+  m->final_norm = take(H);
+  if ((st = init_tensor(m->embed, V, H, 0, 0, H, 0, 0, seed, kTidEmbed, 1.0f, s))) return bail(st);
+  if ((st = init_tensor(m->lm_head, V, H, 0, 0, H, 0, 0, seed, kTidLmHead, s_h, s))) return bail(st);
+  if ((st = fill(m->final_norm, H, 1.0f, s))) return bail(st);
+
+  // ---- paged KV pool
+  m->n_logical_pages = static_cast<int>((c.max_tokens + c.page_tokens - 1) / c.page_tokens);
+  m->n_phys_pages = m->n_logical_pages + std::max(0, c.spare_pages);
+  const size_t page_elems = static_cast<size_t>(m->L) * 2 * m->nkv * c.page_tokens * hd;
+  m->pool_bytes = page_elems * sizeof(bf16) * m->n_phys_pages;
+  if ((st = alloc_dev(reinterpret_cast<void**>(&m->pool), m->pool_bytes))) return bail(st);
+
+  // ---- RoPE table: cos/sin(pos * theta^(-2i/hd)), computed in double.
+  {
+    const long long P = c.max_tokens;
+    const int half = m->hd / 2;
+    std::vector<float2> tab(static_cast<size_t>(P) * half);
+    std::vector<double> inv(half);
+    for (int i = 0; i < half; ++i) inv[i] = std::pow(static_cast<double>(c.rope_theta), -2.0 * i / m->hd);
+    for (long long p = 0; p < P; ++p)
+      for (int i = 0; i < half; ++i) {
+        const double a = static_cast<double>(p) * inv[i];
+        tab[p * half + i] = make_float2(static_cast<float>(std::cos(a)), static_cast<float>(std::sin(a)));
+      }
+    if ((st = alloc_dev(reinterpret_cast<void**>(&m->rope), tab.size() * sizeof(float2)))) return bail(st);
+    cudaError_t e = cudaMemcpy(m->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return bail(fail(CAKE_ECUDA + e, "rope upload: %s", cudaGetErrorString(e)));
+  }
+
+  // ---- activation scratch
+  m->rows_cap = std::max(128, (c.max_chunk + 127) / 128 * 128);
+  const size_t R = m->rows_cap;
+  if ((st = alloc_dev(reinterpret_cast<void**>(&m->h), R * H * sizeof(float)))) return bail(st);
+  if ((st = alloc_dev(reinterpret_cast<void**>(&m->xn), R * H * sizeof(bf16)))) return bail(st);
+  if ((st = alloc_dev(reinterpret_cast<void**>(&m->q), R * m->nq * hd * sizeof(bf16)))) return bail(st);
+  if ((st = alloc_dev(reinterpret_cast<void**>(&m->attn), R * m->nq * hd * sizeof(bf16)))) return bail(st);
+  if ((st = alloc_dev(reinterpret_cast<void**>(&m->act), R * F * sizeof(bf16)))) return bail(st);
+  // split-KV partials: room for 4 splits of a full chunk, or 64 of a short one
+  m->part_rows_cap = std::max<size_t>(4 * R, 64) * m->nq;
+  m->max_splits = 64;
+  if ((st = alloc_dev(reinterpret_cast<void**>(&m->part_o), m->part_rows_cap * hd * sizeof(float)))) return bail(st);
+  if ((st = alloc_dev(reinterpret_cast<void**>(&m->part_lse), m->part_rows_cap * sizeof(float)))) return bail(st);
+  if (c.tp_size > 1 && (st = alloc_dev(reinterpret_cast<void**>(&m->tp_buf), R * H * sizeof(float))))
+    return bail(st);
+  cudaMemset(m->xn, 0, R * H * sizeof(bf16));
+  cudaMemset(m->attn, 0, R * m->nq * hd * sizeof(bf16));
+  cudaMemset(m->act, 0, R * F * sizeof(bf16));
+  if ((st = make_map(&m->a_xn, m->xn, R, H, 128))) return bail(st);
+  if ((st = make_map(&m->a_attn, m->attn, R, m->nq * hd, 128))) return bail(st);
+  if ((st = make_map(&m->a_act, m->act, R, F, 128))) return bail(st);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return bail(fail(CAKE_ECUDA + e, "model init: %s", cudaGetErrorString(e)));
+  *out = m;
+  return CAKE_OK;
+}
+
+int cake_model_get_info(const cake_model* m, cake_model_info* o) {
+  if (!m || !o) return fail(CAKE_EINVAL, "null");
+  o->kv_bytes_per_token = 2LL * m->L * m->nkv * m->hd * 2;
+  o->page_bytes = static_cast<long long>(m->L) * 2 * m->nkv * m->cfg.page_tokens * m->hd * 2;
+  o->n_logical_pages = m->n_logical_pages;
+  o->n_physical_pages = m->n_phys_pages;
+  o->local_q_heads = m->nq;
+  o->local_kv_heads = m->nkv;
+  o->local_ffn = m->F;
+  o->weight_bytes = static_cast<long long>(m->weight_bytes);
+  const long long H = m->H;
+  o->flops_per_token_linear =
+      2LL * m->L * (static_cast<long long>(m->qkv_rows) * H + H * m->nq * m->hd + 2LL * m->F * H + H * m->F);
+  o->kv_pool = m->pool;
+  return CAKE_OK;
+}
+
+int cake_model_set_comm(cake_model* m, void* comm) {
+  m->comm = static_cast<ncclComm_t>(comm);
+  return CAKE_OK;
+}
+
+int cake_model_set_profiling(cake_model* m, int enabled) {
+  m->profiling = enabled != 0;
+  return CAKE_OK;
+}
+
+int cake_model_kernel_stats(cake_model* m, cake_kernel_stat* out, int reset) {
+  for (auto& p : m->prof) {
+    CK(cudaEventSynchronize(p.b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p.a, p.b));
+    cake_kernel_stat& st = m->stats[p.kind];
+    st.launches++;
+    st.total_ms += ms;
+    st.flops += p.flops;
+    st.bytes += p.bytes;
+    m->event_pool.push_back(p.a);
+    m->event_pool.push_back(p.b);
+  }
+  m->prof.clear();
+  if (out) std::memcpy(out, m->stats, sizeof(m->stats));
+  if (reset) std::memset(m->stats, 0, sizeof(m->stats));
+  return CAKE_OK;
+}
+
+int cake_model_launch_count(cake_model* m, long long* n, int reset) {
+  *n = m->launches;
+  if (reset) m->launches = 0;
+  return CAKE_OK;
+}
+
+
+
+int cake_prefill_chunk(cake_model* m, const int32_t* d_tokens, long long chunk_start, int chunk_len,
+                       const int32_t* d_block_table, const int32_t* d_abort, int flags, void* stream) {
+  if (!m) return fail(CAKE_EINVAL, "null model");
+  if (chunk_len < 1 || chunk_len > m->rows_cap) return fail(CAKE_EINVAL, "prefill: chunk_len %d out of range", chunk_len);
+  if (chunk_start < 0 || chunk_start + chunk_len > static_cast<long long>(m->n_logical_pages) * m->cfg.page_tokens)
+    return fail(CAKE_EINVAL, "prefill: chunk beyond KV capacity");
+  if (!(flags & CAKE_PREFILL_NO_KV_WRITE) && chunk_start % m->cfg.page_tokens)
+    return fail(CAKE_EINVAL, "prefill: chunk must start on a page boundary");
+  cudaStream_t s = S(stream);
+  const int M = chunk_len;
+  const int H = m->H;
+  {
+    ProfScope ps(m, CAKE_K_EMBED, s, 0.0, static_cast<double>(M) * H * 6);
+    embed_kernel<<<M, 128, 0, s>>>(d_tokens, m->embed, m->h, H, d_abort);
+    CKL();
+  }
+  const bool no_kv = (flags & CAKE_PREFILL_NO_KV_WRITE) != 0;
+  for (int l = 0; l < m->L; ++l) {
+    LayerWeights& lw = m->layers[l];
+    CKS(rmsnorm(m, lw.ln1, 0, M, d_abort, s));
+    {
+      GemmArgs g{};
+      g.M = M;
+      g.N = no_kv ? m->nq * m->hd : m->qkv_rows;
+      g.K = H;
+      g.q_out = m->q;
+      g.kv_pool = m->pool;
+      g.block_table = d_block_table;
+      g.rope = m->rope;
+      g.pos0 = chunk_start;
+      g.n_q_heads = m->nq;
+      g.n_kv_heads = no_kv ? 0 : m->nkv;
+      g.head_dim = m->hd;
+      g.page_tokens = m->cfg.page_tokens;
+      g.layer = l;
+      g.n_layers = m->L;
+      g.abort_flag = d_abort;
+      if (g.N % m->bn_qkv) return fail(CAKE_EINVAL, "prefill: q-only pass needs tileable q rows");
+      ProfScope ps(m, CAKE_K_GEMM_QKV, s, 2.0 * M * g.N * H, 2.0 * g.N * H + 2.0 * M * H + 2.0 * M * g.N);
+      CKS(gemm_dispatch(m->bn_qkv, kEpiQkv, m->a_xn, lw.m_qkv, g, s));
+    }
+    CKS(attention(m, chunk_start, M, l, d_block_table, d_abort, s));
+    CKS(row_parallel(m, CAKE_K_GEMM_O, m->a_attn, lw.m_o, m->nq * m->hd, M, d_abort, s));
+    CKS(rmsnorm(m, lw.ln2, 0, M, d_abort, s));
+    {
+      GemmArgs g{};
+      g.M = M;
+      g.N = 2 * m->F;
+      g.K = H;
+      g.out = m->act;
+      g.ldo = m->F;
+      g.abort_flag = d_abort;
+      ProfScope ps(m, CAKE_K_GEMM_GU, s, 2.0 * M * g.N * H, 2.0 * g.N * H + 2.0 * M * H + 2.0 * M * m->F);
+      CKS(gemm_dispatch(256, kEpiSwiglu, m->a_xn, lw.m_gu, g, s));
+    }
+    CKS(row_parallel(m, CAKE_K_GEMM_D, m->a_act, lw.m_d, m->F, M, d_abort, s));
+  }
+  return CAKE_OK;
+}
+
+int cake_final_logits(cake_model* m, long long T, const int32_t* d_last_token, int recompute, int last_row,
+                      const int32_t* d_block_table, float* d_logits, void* stream) {
+  cudaStream_t s = S(stream);
+  int row = last_row;
+  if (recompute) {
+    CKS(cake_prefill_chunk(m, d_last_token, T - 1, 1, d_block_table, nullptr, CAKE_PREFILL_NO_KV_WRITE, stream));
+    row = 0;
+  }
+  if (row < 0 || row >= m->rows_cap) return fail(CAKE_EINVAL, "final: bad row");
+  {
+    ProfScope ps(m, CAKE_K_RMSNORM, s, 0.0, m->H * 6.0);
+    rmsnorm_kernel<<<1, 256, 0, s>>>(m->h, m->final_norm, m->xn, m->H, m->cfg.rms_eps, row, nullptr);
+    CKL();
+  }
+  {
+    const int V = m->cfg.vocab;
+    ProfScope ps(m, CAKE_K_LMHEAD, s, 2.0 * V * m->H, 2.0 * V * m->H);
+    const int threads = 256;
+    const int grid = std::min((V + 7) / 8, num_sms() * 4);
+    gemv_kernel<<<grid, threads, m->H * sizeof(float), s>>>(m->lm_head, m->xn, d_logits, V, m->H);
+    CKL();
+  }
+  return CAKE_OK;
+}
+
+long long cake_kv_chunk_bytes(const cake_model* m, int chunk_len) {
+  return 2LL * m->L * m->nkv * m->hd * 2 * chunk_len;
+}
+
+static int kv_permute(cake_model* m, void* staging, long long chunk_start, int chunk_len, const int32_t* bt,
+                      long long b0, long long b1, bool to_pool, cudaStream_t s) {
+  if (chunk_start % m->cfg.page_tokens) return fail(CAKE_EINVAL, "kv: chunk must start on a page boundary");
+  if (b0 % 16 || b1 % 16 || b0 < 0 || b1 > cake_kv_chunk_bytes(m, chunk_len) || b0 > b1)
+    return fail(CAKE_EINVAL, "kv: byte range must be 16-B aligned and inside the chunk");
+  if (b0 == b1) return CAKE_OK;
+  KvLayout L{m->L, m->nkv, m->hd, m->cfg.page_tokens};
+  const unsigned v0 = static_cast<unsigned>(b0 / 16), v1 = static_cast<unsigned>(b1 / 16);
+  const int grid = launch_grid_for(v1 - v0, 256);
+  ProfScope ps(m, CAKE_K_SCATTER, s, 0.0, 2.0 * (b1 - b0));
+  if (to_pool)
+    kv_permute_kernel<true><<<grid, 256, 0, s>>>(static_cast<uint4*>(staging), reinterpret_cast<uint4*>(m->pool), bt,
+                                                 chunk_start / m->cfg.page_tokens, chunk_len, L, v0, v1);
+  else
+    kv_permute_kernel<false><<<grid, 256, 0, s>>>(static_cast<uint4*>(staging), reinterpret_cast<uint4*>(m->pool), bt,
+                                                  chunk_start / m->cfg.page_tokens, chunk_len, L, v0, v1);
+  CKL();
+  return CAKE_OK;
+}
+
+int cake_kv_scatter(cake_model* m, const void* d_staging, long long chunk_start, int chunk_len,
+                    const int32_t* d_block_table, long long byte_begin, long long byte_end, void* stream) {
+  return kv_permute(m, const_cast<void*>(d_staging), chunk_start, chunk_len, d_block_table, byte_begin, byte_end,
+                    true, S(stream));
+}
+
+int cake_kv_gather(cake_model* m, void* d_staging, long long chunk_start, int chunk_len,
+                   const int32_t* d_block_table, void* stream) {
+  return kv_permute(m, d_staging, chunk_start, chunk_len, d_block_table, 0, cake_kv_chunk_bytes(m, chunk_len),
+                    false, S(stream));
+}
+
+int cake_gemm(const void* dA, const void* dB, void* dC, int M, int N, int K, int epi, int block_n, void* stream) {
+  if (M < 1 || N < 1 || K < 64 || K % 64 || N % block_n) return fail(CAKE_EINVAL, "gemm: bad shape");
+  if (epi < 0 || epi > 2) return fail(CAKE_EINVAL, "gemm: epi must be 0..2");
+  CUtensorMap ta, tb;
+  CKS(make_map(&ta, dA, static_cast<uint64_t>(M), static_cast<uint64_t>(K), 128));
+  CKS(make_map(&tb, dB, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint32_t>(block_n)));
+  GemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.out = dC;
+  g.ldo = N;
+  g.resid = static_cast<float*>(dC);
+  g.ldr = N;
+  return gemm_dispatch(block_n, epi, ta, tb, g, S(stream));
+}
+
+}  // extern "C"

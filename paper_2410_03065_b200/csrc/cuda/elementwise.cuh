@@ -1,0 +1,205 @@
+// Memory-bound kernels around the projections: seeded weight init, token
+// embedding, RMSNorm, the last-token LM-head GEMV, and the KV loader's
+// staging <-> paged-cache permutations (scatter for loads, gather to build the
+// cache tier and for debug readback).
+#pragma once
+
+#include "ptx.cuh"
+
+namespace cake_dev {
+
+// ------------------------------------------------------------ seeded init
+// Counter-based generator shared bit-for-bit with the CPU oracle
+// (oracle/llama_ref.c: ref_weight()). Pure integer mixing, then an exact
+// 24-bit fixed-point to float conversion, one fp32 multiply, bf16 RNE.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ float weight_value(uint64_t seed, uint32_t tensor_id,
+                                                       uint64_t logical_index, float scale) {
+  const uint64_t h = mix64(seed ^ mix64((static_cast<uint64_t>(tensor_id) << 40) ^ logical_index));
+  const float u = static_cast<float>(static_cast<int32_t>(h >> 40)) * (1.0f / 8388608.0f) - 1.0f;
+  return u * scale;
+}
+
+// dst is [rows, cols] (row-major, local shard). Physical row r maps to the
+// logical tensor row  (r / group) * group_stride + r % group + row_off  and
+// physical column c to logical column c + col_off of a [*, logical_cols]
+// tensor. group/group_stride express the gate|up interleave of the fused
+// MLP-in weight (group = 128 rows of one tensor per 256-row block).
+struct InitArgs {
+  __nv_bfloat16* dst;
+  long long rows, cols, dst_ld;
+  long long row_off, col_off, logical_cols;
+  long long group, group_stride;  // group = 0: identity row map
+  uint64_t seed;
+  uint32_t tensor_id;
+  float scale;
+};
+
+__global__ void init_weight_kernel(const InitArgs a) {
+  const long long total = a.rows * a.cols;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / a.cols, c = i % a.cols;
+    long long lr = r;
+    if (a.group > 0) lr = (r / a.group) * a.group_stride + (r % a.group);
+    lr += a.row_off;
+    const uint64_t li = static_cast<uint64_t>(lr) * a.logical_cols + (c + a.col_off);
+    a.dst[r * a.dst_ld + c] = __float2bfloat16_rn(weight_value(a.seed, a.tensor_id, li, a.scale));
+  }
+}
+
+__global__ void fill_bf16_kernel(__nv_bfloat16* dst, long long n, float v) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = __float2bfloat16_rn(v);
+}
+
+// ------------------------------------------------------------ embedding
+// h[m, :] = embed[token[m], :] (fp32 residual stream). One CTA per token.
+__global__ void embed_kernel(const int* __restrict__ tokens, const __nv_bfloat16* __restrict__ table,
+                             float* __restrict__ h, int hidden, const int* abort_flag) {
+  if (abort_flag != nullptr && *(volatile const int*)abort_flag) return;
+  const int m = blockIdx.x;
+  const __nv_bfloat16* row = table + static_cast<size_t>(tokens[m]) * hidden;
+  float* out = h + static_cast<size_t>(m) * hidden;
+  for (int i = threadIdx.x * 8; i < hidden; i += blockDim.x * 8) {
+    const uint4 v = *reinterpret_cast<const uint4*>(row + i);
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+    float4 a, b;
+    float2 f0 = __bfloat1622float2(p[0]), f1 = __bfloat1622float2(p[1]);
+    float2 f2 = __bfloat1622float2(p[2]), f3 = __bfloat1622float2(p[3]);
+    a = make_float4(f0.x, f0.y, f1.x, f1.y);
+    b = make_float4(f2.x, f2.y, f3.x, f3.y);
+    *reinterpret_cast<float4*>(out + i) = a;
+    *reinterpret_cast<float4*>(out + i + 4) = b;
+  }
+}
+
+// ------------------------------------------------------------ RMSNorm
+// y[m, :] = bf16( h[m, :] * rsqrt(mean(h^2) + eps) * gamma ). One CTA (256
+// threads) per row; fixed-order reduction (thread-strided partials, shuffle
+// tree, then warps in index order) so results are run-to-run identical.
+__global__ void rmsnorm_kernel(const float* __restrict__ h, const __nv_bfloat16* __restrict__ gamma,
+                               __nv_bfloat16* __restrict__ y, int hidden, float eps, long long row0,
+                               const int* abort_flag) {
+  if (abort_flag != nullptr && *(volatile const int*)abort_flag) return;
+  __shared__ float warp_sums[32];
+  const long long m = row0 + blockIdx.x;
+  const float* x = h + m * hidden;
+  float ss = 0.f;
+  for (int i = threadIdx.x * 4; i < hidden; i += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(x + i);
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+  if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float total = 0.f;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) total += warp_sums[w];
+  const float r = rsqrtf(total / static_cast<float>(hidden) + eps);
+  __nv_bfloat16* out = y + static_cast<long long>(blockIdx.x) * hidden;
+  for (int i = threadIdx.x * 4; i < hidden; i += blockDim.x * 4) {
+    const float4 v = *reinterpret_cast<const float4*>(x + i);
+    const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162*>(gamma + i);
+    const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162*>(gamma + i + 2);
+    const float2 ga = __bfloat1622float2(g01), gb = __bfloat1622float2(g23);
+    uint2 o;
+    o.x = pack_bf16(v.x * r * ga.x, v.y * r * ga.y);
+    o.y = pack_bf16(v.z * r * gb.x, v.w * r * gb.y);
+    *reinterpret_cast<uint2*>(out + i) = o;
+  }
+}
+
+// h += p (tensor-parallel: residual += all-reduced partial sums)
+__global__ void add_inplace_kernel(float* __restrict__ h, const float* __restrict__ p, long long n,
+                                   const int* abort_flag) {
+  if (abort_flag != nullptr && *(volatile const int*)abort_flag) return;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n / 4;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float4 a = reinterpret_cast<float4*>(h)[i];
+    const float4 b = reinterpret_cast<const float4*>(p)[i];
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+    reinterpret_cast<float4*>(h)[i] = a;
+  }
+}
+
+// ------------------------------------------------------------ GEMV (LM head)
+// y[n] = sum_k W[n, k] x[k]; one warp per output row, 16-B loads, x staged
+// in shared memory as fp32. Memory-bound: reads W exactly once.
+__global__ void gemv_kernel(const __nv_bfloat16* __restrict__ W, const __nv_bfloat16* __restrict__ x,
+                            float* __restrict__ y, int N, int K) {
+  extern __shared__ float xs[];
+  for (int i = threadIdx.x; i < K; i += blockDim.x) xs[i] = __bfloat162float(x[i]);
+  __syncthreads();
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int n = blockIdx.x * warps + (threadIdx.x >> 5); n < N; n += gridDim.x * warps) {
+    const __nv_bfloat16* w = W + static_cast<size_t>(n) * K;
+    float acc = 0.f;
+#pragma unroll 4
+    for (int k = lane * 8; k < K; k += 256) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(w + k));
+      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(p[e]);
+        acc += f.x * xs[k + 2 * e] + f.y * xs[k + 2 * e + 1];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, o);
+    if (lane == 0) y[n] = acc;
+  }
+}
+
+// ------------------------------------------------------------ KV loader
+// Cache-tier chunk format (one contiguous range per TP shard):
+//   [layer][K|V][kv_head][token][head_dim] bf16,   token in [0, chunk_len)
+// Paged HBM layout:
+//   pool[phys_page][layer][K|V][kv_head][page_tokens][head_dim]
+// Each thread moves 16-B vectors; consecutive threads walk head_dim then
+// tokens, so both the staging read and the page write are fully coalesced
+// (a page row run is page_tokens*head_dim*2 contiguous bytes).
+struct KvLayout {
+  int n_layers, n_kv_heads, head_dim, page_tokens;
+};
+
+// Chunks start on page boundaries (chunk_size is a multiple of page_tokens),
+// so in-chunk token t lives in logical page first_page + t / page_tokens.
+// In-chunk indices fit 32 bits (a chunk is < 2^31 vectors).
+template <bool kToPool>
+__global__ void kv_permute_kernel(uint4* __restrict__ staging, uint4* __restrict__ pool,
+                                  const int* __restrict__ block_table, long long first_page,
+                                  int chunk_len, KvLayout L, unsigned vec_begin, unsigned vec_end) {
+  const unsigned vpr = static_cast<unsigned>(L.head_dim) / 8u;  // 16-B vectors per token row
+  const unsigned per_plane = static_cast<unsigned>(chunk_len) * vpr;
+  const unsigned page_vecs = static_cast<unsigned>(L.page_tokens) * vpr;
+  const unsigned long long planes_per_page = static_cast<unsigned long long>(L.n_layers) * 2u * L.n_kv_heads;
+  for (unsigned v = vec_begin + blockIdx.x * blockDim.x + threadIdx.x; v < vec_end;
+       v += gridDim.x * blockDim.x) {
+    const unsigned plane = v / per_plane;  // (layer, kv, head) flattened
+    const unsigned rem = v - plane * per_plane;
+    const unsigned t = rem / vpr;
+    const unsigned d = rem - t * vpr;
+    const unsigned pg = t / static_cast<unsigned>(L.page_tokens);
+    const unsigned slot = t - pg * static_cast<unsigned>(L.page_tokens);
+    const unsigned long long phys = static_cast<unsigned long long>(block_table[first_page + pg]);
+    const unsigned long long dst = (phys * planes_per_page + plane) * page_vecs + slot * vpr + d;
+    if (kToPool)
+      pool[dst] = staging[v];
+    else
+      staging[v] = pool[dst];
+  }
+}
+
+}  // namespace cake_dev

@@ -1,0 +1,327 @@
+// Persistent warp-specialised tcgen05 GEMM for the chunk projections.
+//
+//   C[M, N] = A[M, K] · B[N, K]^T     (both operands K-major bf16, fp32 accumulate in TMEM)
+//
+// A is the chunk's activations (M = chunk tokens), B a weight matrix stored
+// [out_features, in_features]. One CTA per SM walks tiles m-fastest so the
+// CTAs that share a weight tile run together and the weight is read from HBM
+// once per chunk. Roles (192 threads):
+//   warp 0      TMA producer: A/B k-blocks into a kStages smem ring (SW128)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..5  epilogue: tcgen05.ld -> fused op -> global
+// Accumulators are double-buffered in TMEM so tile t's epilogue overlaps
+// tile t+1's MMAs.
+//
+// Fused epilogues (the ops that follow each projection in a Llama block):
+//   kEpiBf16    plain bf16 store (tests / generic)
+//   kEpiF32     fp32 store (tensor-parallel partial sums)
+//   kEpiResid   h[m, n] += acc (fp32 residual stream; O-proj and down-proj)
+//   kEpiSwiglu  out[m, j] = silu(gate) * up, gate/up interleaved per 128 cols
+//   kEpiQkv     RoPE on q/k, q -> Q buffer, k/v -> paged KV cache
+#pragma once
+
+#include "ptx.cuh"
+
+namespace cake_dev {
+
+enum GemmEpi : int { kEpiBf16 = 0, kEpiF32 = 1, kEpiResid = 2, kEpiSwiglu = 3, kEpiQkv = 4 };
+
+struct GemmArgs {
+  int M, N, K;
+  int num_m_blocks, num_n_blocks, num_k_blocks;
+  // plain epilogues
+  void* out;  // bf16 or f32
+  int ldo;
+  float* resid;
+  int ldr;
+  // QKV epilogue
+  __nv_bfloat16* q_out;     // [M, n_q * hd]
+  __nv_bfloat16* kv_pool;   // [phys_page][layer][2][n_kv][page_tokens][hd]
+  const int* block_table;   // logical page -> physical page
+  const float2* rope;       // [pos][hd/2] (cos, sin)
+  long long pos0;           // absolute position of row 0
+  int n_q_heads, n_kv_heads, head_dim, page_tokens, layer, n_layers;
+  const int* abort_flag;    // optional: non-zero => skip (lost race / cancelled chunk)
+};
+
+constexpr int kGemmBlockM = 128;
+constexpr int kGemmBlockK = 64;  // 64 bf16 = one 128-B swizzle row
+constexpr int kGemmThreads = 192;
+
+template <int BLOCK_N>
+struct GemmCfg {
+  static constexpr int kABytes = kGemmBlockM * kGemmBlockK * 2;
+  static constexpr int kBBytes = BLOCK_N * kGemmBlockK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (200 * 1024) / kStageBytes;
+  static constexpr int kTmemCols = (2 * BLOCK_N <= 256) ? 256 : 512;
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+
+template <int BLOCK_N, int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                   const __grid_constant__ CUtensorMap tmap_b, const GemmArgs args) {
+  using Cfg = GemmCfg<BLOCK_N>;
+  constexpr int kStages = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+
+  __shared__ int s_abort;
+  if (threadIdx.x == 0) s_abort = (args.abort_flag != nullptr) ? *(volatile const int*)args.abort_flag : 0;
+  __syncthreads();
+  if (s_abort) return;
+
+  const uint32_t raw_base = smem_u32(smem_raw);
+  const uint32_t pad = ((raw_base + 1023u) & ~1023u) - raw_base;
+  uint8_t* smem = smem_raw + pad;
+  uint8_t* smem_a = smem;                                   // [stages][A]
+  uint8_t* smem_b = smem + kStages * Cfg::kABytes;          // [stages][B]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;   // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const uint32_t lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_tiles = args.num_m_blocks * args.num_n_blocks;
+  const int nk = args.num_k_blocks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      const uint64_t pol_w = policy_evict_last();   // weights: reused by the other m-blocks
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m_blk = tile % args.num_m_blocks;
+        const int n_blk = tile / args.num_m_blocks;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1u);
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
+          tma_load_2d(smem_a + stage * Cfg::kABytes, &tmap_a, &full_bar[stage], kb * kGemmBlockK,
+                      m_blk * kGemmBlockM);
+          tma_load_2d_hint(smem_b + stage * Cfg::kBBytes, &tmap_b, &full_bar[stage],
+                           kb * kGemmBlockK, n_blk * BLOCK_N, pol_w);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(kGemmBlockM, BLOCK_N);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BLOCK_N);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem_a + stage * Cfg::kABytes);
+          const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kGemmBlockK / 16; ++k) {
+            umma_bf16_ss(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32),
+                         idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        umma_commit(&tfull_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..5)
+    const int ew = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = ew * 32 + static_cast<int>(lane);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int m_blk = tile % args.num_m_blocks;
+      const int n_blk = tile / args.num_m_blocks;
+      const int m = m_blk * kGemmBlockM + row;
+      const bool valid = m < args.M;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase =
+          tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * BLOCK_N);
+
+      if constexpr (EPI == kEpiBf16 || EPI == kEpiF32 || EPI == kEpiResid) {
+#pragma unroll 1
+        for (int c = 0; c < BLOCK_N / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c * 32, r);
+          tmem_ld_wait();
+          const int n0 = n_blk * BLOCK_N + c * 32;
+          if (valid && n0 < args.N) {
+            if constexpr (EPI == kEpiBf16) {
+              __nv_bfloat16* dst =
+                  reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<size_t>(m) * args.ldo + n0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                st_global_v4(dst + q * 8,
+                             pack_bf16(__uint_as_float(r[q * 8 + 0]), __uint_as_float(r[q * 8 + 1])),
+                             pack_bf16(__uint_as_float(r[q * 8 + 2]), __uint_as_float(r[q * 8 + 3])),
+                             pack_bf16(__uint_as_float(r[q * 8 + 4]), __uint_as_float(r[q * 8 + 5])),
+                             pack_bf16(__uint_as_float(r[q * 8 + 6]), __uint_as_float(r[q * 8 + 7])));
+              }
+            } else if constexpr (EPI == kEpiF32) {
+              float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) +
+                                                      static_cast<size_t>(m) * args.ldo + n0);
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                dst[q] = make_float4(__uint_as_float(r[q * 4]), __uint_as_float(r[q * 4 + 1]),
+                                     __uint_as_float(r[q * 4 + 2]), __uint_as_float(r[q * 4 + 3]));
+            } else {
+              float4* dst =
+                  reinterpret_cast<float4*>(args.resid + static_cast<size_t>(m) * args.ldr + n0);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                float4 h = dst[q];
+                h.x += __uint_as_float(r[q * 4]);
+                h.y += __uint_as_float(r[q * 4 + 1]);
+                h.z += __uint_as_float(r[q * 4 + 2]);
+                h.w += __uint_as_float(r[q * 4 + 3]);
+                dst[q] = h;
+              }
+            }
+          }
+        }
+      } else if constexpr (EPI == kEpiSwiglu) {
+        static_assert(BLOCK_N == 256, "gate/up interleave is 128 columns");
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tbase + c * 32, g);
+          tmem_ld32(tbase + 128 + c * 32, u);
+          tmem_ld_wait();
+          if (valid) {
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) +
+                                 static_cast<size_t>(m) * args.ldo + n_blk * 128 + c * 32;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int i = q * 8 + e * 2;
+                float a0 = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
+                float a1 = silu_f(__uint_as_float(g[i + 1])) * __uint_as_float(u[i + 1]);
+                w[e] = pack_bf16(a0, a1);
+              }
+              st_global_v4(dst + q * 8, w[0], w[1], w[2], w[3]);
+            }
+          }
+        }
+      } else if constexpr (EPI == kEpiQkv) {
+        const int hd = args.head_dim;
+        const int half = hd >> 1;
+        const int heads_per_tile = BLOCK_N / hd;
+        const long long pos = args.pos0 + m;
+#pragma unroll 1
+        for (int h = 0; h < heads_per_tile; ++h) {
+          const int head = n_blk * heads_per_tile + h;
+          const int region = head < args.n_q_heads ? 0 : (head < args.n_q_heads + args.n_kv_heads ? 1 : 2);
+#pragma unroll 1
+          for (int j = 0; j < half / 32; ++j) {
+            uint32_t x0[32], x1[32];
+            tmem_ld32(tbase + h * hd + j * 32, x0);
+            tmem_ld32(tbase + h * hd + half + j * 32, x1);
+            tmem_ld_wait();
+            if (!valid) continue;
+            float o0[32], o1[32];
+            if (region < 2) {
+              const float2* cs = args.rope + pos * half + j * 32;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float2 t = cs[i];
+                const float a = __uint_as_float(x0[i]);
+                const float b = __uint_as_float(x1[i]);
+                o0[i] = a * t.x - b * t.y;
+                o1[i] = b * t.x + a * t.y;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                o0[i] = __uint_as_float(x0[i]);
+                o1[i] = __uint_as_float(x1[i]);
+              }
+            }
+            __nv_bfloat16* dst;
+            if (region == 0) {
+              dst = args.q_out + static_cast<size_t>(m) * (args.n_q_heads * hd) + head * hd;
+            } else {
+              const int kvh = region == 1 ? head - args.n_q_heads : head - args.n_q_heads - args.n_kv_heads;
+              const long long lpage = pos / args.page_tokens;
+              const int slot = static_cast<int>(pos - lpage * args.page_tokens);
+              const long long phys = args.block_table[lpage];
+              const size_t off =
+                  ((((static_cast<size_t>(phys) * args.n_layers + args.layer) * 2 + (region - 1)) *
+                        args.n_kv_heads + kvh) * args.page_tokens + slot) * static_cast<size_t>(hd);
+              dst = args.kv_pool + off;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              st_global_v4(dst + j * 32 + q * 8, pack_bf16(o0[q * 8 + 0], o0[q * 8 + 1]),
+                           pack_bf16(o0[q * 8 + 2], o0[q * 8 + 3]), pack_bf16(o0[q * 8 + 4], o0[q * 8 + 5]),
+                           pack_bf16(o0[q * 8 + 6], o0[q * 8 + 7]));
+              st_global_v4(dst + half + j * 32 + q * 8, pack_bf16(o1[q * 8 + 0], o1[q * 8 + 1]),
+                           pack_bf16(o1[q * 8 + 2], o1[q * 8 + 3]), pack_bf16(o1[q * 8 + 4], o1[q * 8 + 5]),
+                           pack_bf16(o1[q * 8 + 6], o1[q * 8 + 7]));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace cake_dev
