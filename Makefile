@@ -9,7 +9,7 @@ PKG     := paper_2410_03065_b200
 LIB     := $(PKG)/_lib
 INC     := -Iinclude
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden -Xptxas -v $(INC)
-CXXFLAGS:= -O3 -std=c++20 -fPIC -fvisibility=hidden -Wall -Wextra -Wno-unused-parameter $(INC) -I/usr/local/cuda/include
+CXXFLAGS:= -O3 -std=c++20 -fPIC -Wall -Wextra -Wno-unused-parameter $(INC) -I/usr/local/cuda/include
 CUDA_LIBDIR := /usr/local/cuda/lib64
 
 CUDA_SRC := $(PKG)/csrc/cuda/cake_cuda.cu

@@ -131,6 +131,13 @@ enum {
 CAKE_API int cake_prefill_chunk(cake_model* m, const int32_t* d_tokens, long long chunk_start, int chunk_len,
                        const int32_t* d_block_table, const int32_t* d_abort, int flags, void* stream);
 
+/* Layers [layer_begin, layer_end) of one chunk (embedding runs with layer 0).
+ * Lets the host record an event a few layers before the end of a chunk, which
+ * is when the scheduler claims the next one. */
+CAKE_API int cake_prefill_layers(cake_model* m, const int32_t* d_tokens, long long chunk_start, int chunk_len,
+                                 int layer_begin, int layer_end, const int32_t* d_block_table,
+                                 const int32_t* d_abort, int flags, void* stream);
+
 /* First-token logits (fp32 [vocab]) of a prompt of T tokens whose KV is fully
  * resident. recompute = 1: run the last token as a 1-row q-only pass over the
  * cache (needed when the tail chunk was loaded, not computed); recompute = 0:

@@ -196,6 +196,7 @@ struct cake_model {
   CUtensorMap a_xn, a_attn, a_act;
   ncclComm_t comm = nullptr;
   bool profiling = false;
+  std::mutex prof_mu;  // launches come from the compute thread and the loader's pacer thread
   std::vector<ProfPair> prof;
   std::vector<cudaEvent_t> event_pool;
   cake_kernel_stat stats[CAKE_K_COUNT]{};
@@ -224,6 +225,7 @@ struct ProfScope {
   cudaEvent_t a = nullptr;
   ProfScope(cake_model* m_, int kind_, cudaStream_t s_, double f, double b)
       : m(m_), kind(kind_), s(s_), flops(f), bytes(b) {
+    std::lock_guard<std::mutex> g(m->prof_mu);
     m->launches++;
     if (m->profiling) {
       a = pool_event(m);
@@ -231,7 +233,8 @@ struct ProfScope {
     }
   }
   ~ProfScope() {
-    if (m->profiling) {
+    if (a != nullptr) {
+      std::lock_guard<std::mutex> g(m->prof_mu);
       cudaEvent_t b = pool_event(m);
       cudaEventRecord(b, s);
       m->prof.push_back({kind, a, b, flops, bytes});
@@ -712,6 +715,7 @@ int cake_model_set_profiling(cake_model* m, int enabled) {
 }
 
 int cake_model_kernel_stats(cake_model* m, cake_kernel_stat* out, int reset) {
+  std::lock_guard<std::mutex> g(m->prof_mu);
   for (auto& p : m->prof) {
     CK(cudaEventSynchronize(p.b));
     float ms = 0.f;
@@ -731,6 +735,7 @@ int cake_model_kernel_stats(cake_model* m, cake_kernel_stat* out, int reset) {
 }
 
 int cake_model_launch_count(cake_model* m, long long* n, int reset) {
+  std::lock_guard<std::mutex> g(m->prof_mu);
   *n = m->launches;
   if (reset) m->launches = 0;
   return CAKE_OK;
@@ -741,6 +746,14 @@ int cake_model_launch_count(cake_model* m, long long* n, int reset) {
 int cake_prefill_chunk(cake_model* m, const int32_t* d_tokens, long long chunk_start, int chunk_len,
                        const int32_t* d_block_table, const int32_t* d_abort, int flags, void* stream) {
   if (!m) return fail(CAKE_EINVAL, "null model");
+  return cake_prefill_layers(m, d_tokens, chunk_start, chunk_len, 0, m->L, d_block_table, d_abort, flags, stream);
+}
+
+int cake_prefill_layers(cake_model* m, const int32_t* d_tokens, long long chunk_start, int chunk_len, int layer_begin,
+                        int layer_end, const int32_t* d_block_table, const int32_t* d_abort, int flags,
+                        void* stream) {
+  if (!m) return fail(CAKE_EINVAL, "null model");
+  if (layer_begin < 0 || layer_end > m->L || layer_begin >= layer_end) return fail(CAKE_EINVAL, "prefill: bad layer range");
   if (chunk_len < 1 || chunk_len > m->rows_cap) return fail(CAKE_EINVAL, "prefill: chunk_len %d out of range", chunk_len);
   if (chunk_start < 0 || chunk_start + chunk_len > static_cast<long long>(m->n_logical_pages) * m->cfg.page_tokens)
     return fail(CAKE_EINVAL, "prefill: chunk beyond KV capacity");
@@ -749,13 +762,13 @@ int cake_prefill_chunk(cake_model* m, const int32_t* d_tokens, long long chunk_s
   cudaStream_t s = S(stream);
   const int M = chunk_len;
   const int H = m->H;
-  {
+  if (layer_begin == 0) {
     ProfScope ps(m, CAKE_K_EMBED, s, 0.0, static_cast<double>(M) * H * 6);
     embed_kernel<<<M, 128, 0, s>>>(d_tokens, m->embed, m->h, H, d_abort);
     CKL();
   }
   const bool no_kv = (flags & CAKE_PREFILL_NO_KV_WRITE) != 0;
-  for (int l = 0; l < m->L; ++l) {
+  for (int l = layer_begin; l < layer_end; ++l) {
     LayerWeights& lw = m->layers[l];
     CKS(rmsnorm(m, lw.ln1, 0, M, d_abort, s));
     {

@@ -1,0 +1,652 @@
+// GPU runtime: GpuContext, the compute-side PrefillBackend, the loader-side
+// ChunkSink, the race-to-finish commit protocol and the live bidirectional
+// run that replaces reference run_live (proj/src/scheduler.cpp:229-278).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <thread>
+
+#include "cake/gpu.hpp"
+#include "cake_cuda.h"
+#include "internal.hpp"
+
+namespace cake {
+
+namespace {
+
+void check(int st, const char* what) {
+  if (st == CAKE_OK) return;
+  char buf[768];
+  cake_cuda_last_error(buf, sizeof buf);
+  throw std::runtime_error(std::string(what) + ": " + buf + " (status " + std::to_string(st) + ")");
+}
+
+void* pinned_alloc(std::size_t n, void*) {
+  void* p = nullptr;
+  return cake_host_alloc(&p, n) == CAKE_OK ? p : nullptr;
+}
+void pinned_release(void* p, void*) { cake_host_free(p); }
+
+struct Event {
+  void* h = nullptr;
+  Event() { check(cake_event_create(&h, 1), "cudaEventCreate"); }
+  ~Event() {
+    if (h) cake_event_destroy(h);
+  }
+  Event(const Event&) = delete;
+  Event& operator=(const Event&) = delete;
+};
+
+template <typename T>
+struct Pinned {
+  T* p = nullptr;
+  std::size_t n = 0;
+  void reset(std::size_t count) {
+    release();
+    n = count;
+    void* v = nullptr;
+    check(cake_host_alloc(&v, std::max<std::size_t>(1, count) * sizeof(T)), "pinned alloc");
+    p = static_cast<T*>(v);
+  }
+  void release() {
+    if (p) cake_host_free(p);
+    p = nullptr;
+  }
+  ~Pinned() { release(); }
+};
+
+template <typename T>
+struct Device {
+  T* p = nullptr;
+  void reset(std::size_t count) {
+    release();
+    void* v = nullptr;
+    check(cake_dev_alloc(&v, std::max<std::size_t>(1, count) * sizeof(T)), "device alloc");
+    p = static_cast<T*>(v);
+  }
+  void release() {
+    if (p) cake_dev_free(p);
+    p = nullptr;
+  }
+  ~Device() { release(); }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ presets
+GpuModelConfig GpuModelConfig::llama3_8b() {
+  return {"llama-3-8b", 32, 4096, 32, 8, 128, 14336, 128256, 500000.0f, 1e-5f, 64};
+}
+GpuModelConfig GpuModelConfig::llama3_70b() {
+  return {"llama-3-70b", 80, 8192, 64, 8, 128, 28672, 128256, 500000.0f, 1e-5f, 64};
+}
+GpuModelConfig GpuModelConfig::tiny() { return {"tiny", 2, 256, 4, 4, 64, 1024, 32000, 500000.0f, 1e-5f, 64}; }
+
+ModelProfile GpuModelConfig::profile(int tp_size) const {
+  ModelProfile p;
+  p.name = name;
+  p.n_layers = static_cast<std::uint32_t>(n_layers);
+  p.hidden_size = static_cast<std::uint32_t>(n_kv_heads / tp_size * head_dim);  // KV width (GQA)
+  p.precision_bytes = 2;
+  p.kv_multiplier = 2;
+  return p;
+}
+
+// ------------------------------------------------------------------ context
+struct GpuContext::Impl {
+  GpuModelConfig cfg;
+  GpuOptions opt;
+  cake_model* model = nullptr;
+  cake_model_info info{};
+  void* s_compute = nullptr;
+  void* s_copy = nullptr;
+  void* s_control = nullptr;
+  int n_pages = 0;        // logical pages
+  int spare_pages = 0;    // second page set for one contested chunk
+  Device<std::int32_t> bt_primary, bt_race, tokens, abort_flags;
+  Pinned<std::int32_t> h_bt_race, h_tokens, h_abort_one;
+  Device<std::byte> staging[2];
+  std::size_t staging_bytes = 0;
+  Device<float> logits;
+  Pinned<float> h_logits;
+  const std::int32_t* final_bt = nullptr;
+  std::vector<std::unique_ptr<Event>> ev_start, ev_near, ev_end, ev_io;
+  std::unique_ptr<Event> ev_anchor, ev_copy_done, ev_final_start, ev_logits;  // created after set_device
+  GpuRunInfo last;
+
+  void ensure_events(std::size_t n) {
+    for (auto* v : {&ev_start, &ev_near, &ev_end, &ev_io})
+      while (v->size() < n) v->push_back(std::make_unique<Event>());
+  }
+  int pages_of(const ChunkSpec& c) const {
+    return static_cast<int>((c.token_count + cfg.page_tokens - 1) / cfg.page_tokens);
+  }
+};
+
+GpuContext::GpuContext(const GpuModelConfig& cfg, const GpuOptions& opt) : impl_(std::make_unique<Impl>()) {
+  Impl& g = *impl_;
+  g.cfg = cfg;
+  g.opt = opt;
+  check(cake_cuda_set_device(opt.device), "set device");
+  if (opt.max_chunk % cfg.page_tokens) throw std::invalid_argument("gpu: max_chunk must be a multiple of page_tokens");
+  cake_model_config mc{};
+  mc.n_layers = cfg.n_layers;
+  mc.hidden = cfg.hidden;
+  mc.n_heads = cfg.n_heads;
+  mc.n_kv_heads = cfg.n_kv_heads;
+  mc.head_dim = cfg.head_dim;
+  mc.ffn = cfg.ffn;
+  mc.vocab = cfg.vocab;
+  mc.rope_theta = cfg.rope_theta;
+  mc.rms_eps = cfg.rms_eps;
+  mc.page_tokens = cfg.page_tokens;
+  mc.max_chunk = opt.max_chunk;
+  mc.max_tokens = opt.max_tokens;
+  g.spare_pages = opt.max_chunk / cfg.page_tokens;
+  mc.spare_pages = g.spare_pages;
+  mc.tp_rank = opt.tp_rank;
+  mc.tp_size = opt.tp_size;
+  mc.seed = opt.weight_seed;
+  g.ev_anchor = std::make_unique<Event>();
+  g.ev_copy_done = std::make_unique<Event>();
+  g.ev_final_start = std::make_unique<Event>();
+  g.ev_logits = std::make_unique<Event>();
+  check(cake_model_create(&mc, &g.model), "model create");
+  check(cake_model_get_info(g.model, &g.info), "model info");
+  if (opt.tp_size > 1) {
+    if (!opt.nccl_comm) throw std::invalid_argument("gpu: tp_size > 1 needs an NCCL communicator");
+    check(cake_model_set_comm(g.model, opt.nccl_comm), "set comm");
+  }
+  check(cake_model_set_profiling(g.model, opt.profile_kernels ? 1 : 0), "profiling");
+  check(cake_stream_create(&g.s_compute, 0), "stream");
+  check(cake_stream_create(&g.s_copy, 1), "stream");     // loader work jumps the queue for free SMs
+  check(cake_stream_create(&g.s_control, 1), "stream");
+  g.n_pages = g.info.n_logical_pages;
+  g.bt_primary.reset(g.n_pages);
+  g.bt_race.reset(g.n_pages);
+  g.h_bt_race.reset(g.n_pages);
+  for (int i = 0; i < g.n_pages; ++i) g.h_bt_race.p[i] = i;  // identity: logical page i -> physical i
+  check(cake_h2d_async(g.bt_primary.p, g.h_bt_race.p, g.n_pages * sizeof(std::int32_t), g.s_compute), "bt upload");
+  check(cake_h2d_async(g.bt_race.p, g.h_bt_race.p, g.n_pages * sizeof(std::int32_t), g.s_compute), "bt upload");
+  g.tokens.reset(static_cast<std::size_t>(opt.max_tokens));
+  g.h_tokens.reset(static_cast<std::size_t>(opt.max_tokens));
+  g.abort_flags.reset(g.n_pages);
+  g.h_abort_one.reset(1);
+  g.h_abort_one.p[0] = 1;
+  g.staging_bytes = static_cast<std::size_t>(cake_kv_chunk_bytes(g.model, opt.max_chunk));
+  g.staging[0].reset(g.staging_bytes);
+  g.staging[1].reset(g.staging_bytes);
+  g.logits.reset(cfg.vocab);
+  g.h_logits.reset(cfg.vocab);
+  g.final_bt = g.bt_primary.p;
+  check(cake_stream_sync(g.s_compute), "init sync");
+}
+
+GpuContext::~GpuContext() {
+  Impl& g = *impl_;
+  cake_cuda_device_sync();
+  for (void* s : {g.s_compute, g.s_copy, g.s_control})
+    if (s) cake_stream_destroy(s);
+  if (g.model) cake_model_destroy(g.model);
+}
+
+cake_model* GpuContext::model() const { return impl_->model; }
+void* GpuContext::compute_stream() const { return impl_->s_compute; }
+void* GpuContext::copy_stream() const { return impl_->s_copy; }
+void* GpuContext::control_stream() const { return impl_->s_control; }
+HostAllocator GpuContext::pinned_allocator() const { return {pinned_alloc, pinned_release, nullptr}; }
+const GpuModelConfig& GpuContext::config() const { return impl_->cfg; }
+const GpuOptions& GpuContext::options() const { return impl_->opt; }
+std::uint64_t GpuContext::kv_bytes_per_token() const {
+  return static_cast<std::uint64_t>(impl_->info.kv_bytes_per_token);
+}
+int GpuContext::page_tokens() const { return impl_->cfg.page_tokens; }
+const GpuRunInfo& GpuContext::last_run() const { return impl_->last; }
+
+namespace {
+
+void check_chunking(const GpuContext::Impl& g, std::span<const ChunkSpec> chunks, std::uint64_t total) {
+  if (total > static_cast<std::uint64_t>(g.opt.max_tokens)) throw std::invalid_argument("gpu: prompt exceeds max_tokens");
+  for (const ChunkSpec& c : chunks) {
+    if (c.token_count > static_cast<std::uint32_t>(g.opt.max_chunk))
+      throw std::invalid_argument("gpu: chunk exceeds max_chunk");
+    if (c.token_start % g.cfg.page_tokens)
+      throw std::invalid_argument("gpu: chunk_size must be a multiple of page_tokens (" +
+                                  std::to_string(g.cfg.page_tokens) + ")");
+  }
+}
+
+void upload_tokens(GpuContext::Impl& g, const std::vector<std::uint32_t>& ids, void* stream) {
+  for (std::size_t i = 0; i < ids.size(); ++i) g.h_tokens.p[i] = static_cast<std::int32_t>(ids[i]);
+  check(cake_h2d_async(g.tokens.p, g.h_tokens.p, ids.size() * sizeof(std::int32_t), stream), "tokens H2D");
+}
+
+}  // namespace
+
+PopulateResult GpuContext::build_cache_tier(ChunkStore& store, const RequestSpec& request, std::uint64_t prompt_seed) {
+  Impl& g = *impl_;
+  request.validate();
+  const auto chunks = split_into_chunks(request.total_tokens, request.chunk_size);
+  check_chunking(g, chunks, request.total_tokens);
+  const auto ids = token_stream(prompt_seed, request.total_tokens);
+  upload_tokens(g, ids, g.s_compute);
+  check(cake_memset_async(g.abort_flags.p, 0, g.n_pages * sizeof(std::int32_t), g.s_compute), "memset");
+  const ModelProfile prof = g.cfg.profile(g.opt.tp_size);
+  Pinned<std::byte> host;
+  host.reset(g.staging_bytes);
+  PopulateResult res;
+  std::optional<ChunkKey> prev;
+  for (const ChunkSpec& c : chunks) {
+    check(cake_prefill_chunk(g.model, g.tokens.p + c.token_start, static_cast<long long>(c.token_start),
+                             static_cast<int>(c.token_count), g.bt_primary.p, nullptr, 0, g.s_compute),
+          "prefill");
+    const auto bytes = static_cast<std::size_t>(cake_kv_chunk_bytes(g.model, static_cast<int>(c.token_count)));
+    check(cake_kv_gather(g.model, g.staging[0].p, static_cast<long long>(c.token_start), static_cast<int>(c.token_count),
+                         g.bt_primary.p, g.s_compute),
+          "gather");
+    check(cake_d2h_async(host.p, g.staging[0].p, bytes, g.s_compute), "D2H");
+    check(cake_stream_sync(g.s_compute), "sync");
+    const ChunkKey key =
+        chain_hash(prev, std::span<const std::uint32_t>(ids.data() + c.token_start, c.token_count));
+    prev = key;
+    res.keys.push_back(key);
+    if (bytes != chunk_bytes(prof, c)) throw std::logic_error("gpu: chunk bytes disagree with the KV profile");
+    const ChunkMeta meta{c.token_count, "identity", bytes, bytes};
+    if (store.contains(key)) {
+      ++res.chunks_existing;
+      continue;
+    }
+    store.put(key, std::span<const std::byte>(host.p, bytes), meta);
+    res.bytes_written += bytes;
+    ++res.chunks_written;
+  }
+  return res;
+}
+
+CostModel GpuContext::calibrate(const RequestSpec& request, std::uint64_t prompt_seed) {
+  Impl& g = *impl_;
+  request.validate();
+  const auto chunks = split_into_chunks(request.total_tokens, request.chunk_size);
+  check_chunking(g, chunks, request.total_tokens);
+  upload_tokens(g, token_stream(prompt_seed, request.total_tokens), g.s_compute);
+  check(cake_memset_async(g.abort_flags.p, 0, g.n_pages * sizeof(std::int32_t), g.s_compute), "memset");
+  g.ensure_events(chunks.size());
+  for (const ChunkSpec& c : chunks) {
+    check(cake_event_record(g.ev_start[c.index]->h, g.s_compute), "record");
+    check(cake_prefill_chunk(g.model, g.tokens.p + c.token_start, static_cast<long long>(c.token_start),
+                             static_cast<int>(c.token_count), g.bt_primary.p, nullptr, 0, g.s_compute),
+          "prefill");
+    check(cake_event_record(g.ev_end[c.index]->h, g.s_compute), "record");
+  }
+  check(cake_stream_sync(g.s_compute), "sync");
+  // least squares  d_i = a + b * start_i  over full-size chunks (scaled by size otherwise)
+  double sx = 0, sy = 0, sxx = 0, sxy = 0;
+  int n = 0;
+  for (const ChunkSpec& c : chunks) {
+    float ms = 0.f;
+    check(cake_event_elapsed_ms(g.ev_start[c.index]->h, g.ev_end[c.index]->h, &ms), "elapsed");
+    const double y = static_cast<double>(ms) * request.chunk_size / c.token_count;
+    const double x = static_cast<double>(c.token_start);
+    sx += x;
+    sy += y;
+    sxx += x * x;
+    sxy += x * y;
+    ++n;
+  }
+  double b = 0.0, a = sy / n;
+  const double den = n * sxx - sx * sx;
+  if (n > 1 && den > 0) {
+    b = (n * sxy - sx * sy) / den;
+    a = (sy - b * sx) / n;
+  }
+  CostModel cm{std::max(0.0, a), std::max(0.0, b), request.chunk_size};
+  g.opt.prior = cm;
+  return cm;
+}
+
+std::vector<std::byte> GpuContext::read_chunk_kv(const ChunkSpec& chunk) const {
+  Impl& g = *impl_;
+  const auto bytes = static_cast<std::size_t>(cake_kv_chunk_bytes(g.model, static_cast<int>(chunk.token_count)));
+  check(cake_kv_gather(g.model, g.staging[0].p, static_cast<long long>(chunk.token_start),
+                       static_cast<int>(chunk.token_count), g.final_bt, g.s_compute),
+        "gather");
+  std::vector<std::byte> out(bytes);
+  Pinned<std::byte> host;
+  host.reset(bytes);
+  check(cake_d2h_async(host.p, g.staging[0].p, bytes, g.s_compute), "D2H");
+  check(cake_stream_sync(g.s_compute), "sync");
+  std::memcpy(out.data(), host.p, bytes);
+  return out;
+}
+
+// ================================================================== live run
+namespace {
+
+constexpr int kNone = 0, kByCompute = 1, kByIo = 2;
+
+// State one bidirectional run shares between the compute thread, the
+// loader's pacer/completion threads and the final step.
+struct LiveRun {
+  GpuContext::Impl& g;
+  const RunPlan& plan;
+  const RunTimer& timer;
+  Micros t0 = 0;  // run clock at the anchor event
+  std::unique_ptr<std::atomic<int>[]> commit;
+  std::atomic<int> race_chunk{-1};
+  std::atomic<int> racer{-1};  // kByCompute / kByIo
+  TransferEngine* loader = nullptr;
+
+  LiveRun(GpuContext::Impl& g_, const RunPlan& p, const RunTimer& t) : g(g_), plan(p), timer(t) {
+    commit = std::make_unique<std::atomic<int>[]>(p.chunks.size());
+    for (std::size_t i = 0; i < p.chunks.size(); ++i) commit[i].store(kNone);
+  }
+
+  Micros device_time(void* ev) const {
+    float ms = 0.f;
+    check(cake_event_elapsed_ms(g.ev_anchor->h, ev, &ms), "elapsed");
+    return t0 + static_cast<Micros>(std::llround(static_cast<double>(ms) * 1000.0));
+  }
+
+  bool try_commit(std::uint32_t i, int who) {
+    int expected = kNone;
+    return commit[i].compare_exchange_strong(expected, who);
+  }
+
+  // Second page set for contested chunk k, uploaded on the racer's stream
+  // ahead of the racer's writes.
+  void start_race(const ChunkSpec& c, int who, void* stream) {
+    race_chunk.store(static_cast<int>(c.index));
+    racer.store(who);
+    const int first = static_cast<int>(c.token_start / g.cfg.page_tokens);
+    for (int p = 0; p < g.n_pages; ++p) g.h_bt_race.p[p] = p;
+    for (int p = 0; p < g.pages_of(c); ++p) g.h_bt_race.p[first + p] = g.n_pages + p;
+    check(cake_h2d_async(g.bt_race.p, g.h_bt_race.p, g.n_pages * sizeof(std::int32_t), stream), "race bt");
+  }
+
+  // Which page table each side writes a chunk through.
+  const std::int32_t* table_for(std::uint32_t i, int who) const {
+    return (race_chunk.load() == static_cast<int>(i) && racer.load() == who) ? g.bt_race.p : g.bt_primary.p;
+  }
+
+  void abort_compute(std::uint32_t i) {
+    check(cake_h2d_async(g.abort_flags.p + i, g.h_abort_one.p, sizeof(std::int32_t), g.s_control), "abort");
+  }
+};
+
+class GpuPrefillBackend final : public PrefillBackend {
+ public:
+  GpuPrefillBackend(LiveRun& run, const CostModel& prior) : r_(run), prior_(prior) {}
+
+  void pace() override {
+    if (launched_.empty()) return;
+    check(cake_event_sync(r_.g.ev_near[launched_.back()]->h), "pace");
+    observe();
+  }
+
+  void launch(const ChunkSpec& c, bool contested) override {
+    GpuContext::Impl& g = r_.g;
+    const Micros predicted = predict_finish(c);
+    if (contested) r_.start_race(c, kByCompute, g.s_compute);
+    const std::int32_t* bt = r_.table_for(c.index, kByCompute);
+    const int L = g.cfg.n_layers;
+    const int split = std::clamp(L - g.opt.lookahead_layers, 1, L);
+    const auto start = static_cast<long long>(c.token_start);
+    const auto len = static_cast<int>(c.token_count);
+    const std::int32_t* tok = g.tokens.p + c.token_start;
+    const std::int32_t* abort = g.abort_flags.p + c.index;
+    check(cake_event_record(g.ev_start[c.index]->h, g.s_compute), "record");
+    check(cake_prefill_layers(g.model, tok, start, len, 0, split, bt, abort, 0, g.s_compute), "prefill");
+    check(cake_event_record(g.ev_near[c.index]->h, g.s_compute), "record");
+    if (split < L) check(cake_prefill_layers(g.model, tok, start, len, split, L, bt, abort, 0, g.s_compute), "prefill");
+    check(cake_event_record(g.ev_end[c.index]->h, g.s_compute), "record");
+    std::lock_guard lk(mu_);
+    launched_.push_back(c.index);
+    predicted_end_.push_back(predicted);
+  }
+
+  Micros predict_finish(const ChunkSpec& c) override {
+    const Micros now = r_.timer.now_us();
+    const Micros free_at = launched_.empty() ? now : expected_end(launched_.size() - 1);
+    return std::max(now, free_at) + duration(c);
+  }
+
+  // Predicted completion of launched chunk `index` (for the loader's race policy).
+  std::optional<Micros> expected_end_of(std::uint32_t index) {
+    std::lock_guard lk(mu_);
+    for (std::size_t k = 0; k < launched_.size(); ++k)
+      if (launched_[k] == index) return expected_end(k);
+    return std::nullopt;
+  }
+
+  std::vector<ChunkRecord> drain() override {
+    std::vector<ChunkRecord> out;
+    for (std::uint32_t i : launched_) {
+      check(cake_event_sync(r_.g.ev_end[i]->h), "drain");
+      if (!r_.try_commit(i, kByCompute)) continue;  // the loader landed it first
+      out.push_back({i, Side::compute, r_.device_time(r_.g.ev_start[i]->h), r_.device_time(r_.g.ev_end[i]->h), 0});
+    }
+    last_launched_ = launched_.empty() ? -1 : static_cast<int>(launched_.back());
+    return out;
+  }
+
+  int last_launched() const { return last_launched_; }
+
+ private:
+  Micros duration(const ChunkSpec& c) const {
+    const double base = static_cast<double>(compute_latency(prior_, c, 1.0));
+    const double ratio = den_ > 0 ? num_ / den_ : 1.0;
+    return static_cast<Micros>(base * ratio);
+  }
+  Micros expected_end(std::size_t k) const {
+    const std::uint32_t i = launched_[k];
+    if (cake_event_query(r_.g.ev_end[i]->h) == CAKE_OK) return r_.device_time(r_.g.ev_end[i]->h);
+    if (cake_event_query(r_.g.ev_start[i]->h) == CAKE_OK)
+      return r_.device_time(r_.g.ev_start[i]->h) + duration(r_.plan.chunks[i]);
+    return predicted_end_[k];
+  }
+  // Fold finished chunks into the observed/prior duration ratio.
+  void observe() {
+    while (observed_ < launched_.size()) {
+      const std::uint32_t i = launched_[observed_];
+      if (cake_event_query(r_.g.ev_end[i]->h) != CAKE_OK) break;
+      float ms = 0.f;
+      check(cake_event_elapsed_ms(r_.g.ev_start[i]->h, r_.g.ev_end[i]->h, &ms), "elapsed");
+      num_ += static_cast<double>(ms) * 1000.0;
+      den_ += static_cast<double>(compute_latency(prior_, r_.plan.chunks[i], 1.0));
+      ++observed_;
+    }
+  }
+
+  LiveRun& r_;
+  CostModel prior_;
+  std::mutex mu_;
+  std::vector<std::uint32_t> launched_;
+  std::vector<Micros> predicted_end_;
+  std::size_t observed_ = 0;
+  double num_ = 0.0, den_ = 0.0;
+  int last_launched_ = -1;
+};
+
+class GpuLoaderSink final : public ChunkSink {
+ public:
+  explicit GpuLoaderSink(LiveRun& run) : r_(run) {}
+
+  void begin_chunk(const FetchTask& t) override {
+    GpuContext::Impl& g = r_.g;
+    if (t.contested) r_.start_race(t.chunk, kByIo, g.s_copy);
+    buf_ = g.staging[parity_].p;
+    parity_ ^= 1;
+  }
+
+  void deliver(const FetchTask& t, std::uint64_t offset, std::span<const std::byte> bytes) override {
+    check(cake_h2d_async(buf_ + offset, bytes.data(), bytes.size(), r_.g.s_copy), "slice H2D");
+    h2d_bytes_ += bytes.size();
+  }
+
+  void end_chunk(const FetchTask& t) override {
+    GpuContext::Impl& g = r_.g;
+    check(cake_kv_scatter(g.model, buf_, static_cast<long long>(t.chunk.token_start), static_cast<int>(t.chunk.token_count),
+                          r_.table_for(t.chunk.index, kByIo), 0, static_cast<long long>(t.encoded_bytes), g.s_copy),
+          "scatter");
+    check(cake_event_record(g.ev_io[t.chunk.index]->h, g.s_copy), "record");
+  }
+
+  Micros wait_chunk(const FetchTask& t) override {
+    check(cake_event_sync(r_.g.ev_io[t.chunk.index]->h), "io wait");
+    if (!r_.try_commit(t.chunk.index, kByIo)) return -1;  // compute landed it first
+    r_.abort_compute(t.chunk.index);  // stop any compute work still queued for it
+    return r_.device_time(r_.g.ev_io[t.chunk.index]->h);
+  }
+
+  bool keep_going(const FetchTask& t) override { return r_.commit[t.chunk.index].load() != kByCompute; }
+
+  HostAllocator staging_allocator() override { return {pinned_alloc, pinned_release, nullptr}; }
+
+  std::uint64_t h2d_bytes() const { return h2d_bytes_; }
+
+ private:
+  LiveRun& r_;
+  std::byte* buf_ = nullptr;
+  int parity_ = 0;
+  std::uint64_t h2d_bytes_ = 0;
+};
+
+}  // namespace
+
+namespace detail {
+
+RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& tokens, const CostModel& cost,
+                       const BandwidthTrace& trace, const Codec& codec, const ChunkStore& store, RunMode mode,
+                       double power, const RunOptions& opt) {
+  GpuContext::Impl& g = *opt.gpu->impl();
+  if (codec.kind != Codec::Kind::identity) throw std::invalid_argument("gpu run: only the identity codec is wired");
+  const auto n = static_cast<std::uint32_t>(plan.chunks.size());
+  check_chunking(g, plan.chunks, tokens.size());
+  for (std::uint32_t i = 0; i < n; ++i)
+    if (plan.encoded_bytes[i] != static_cast<std::uint64_t>(cake_kv_chunk_bytes(g.model, plan.chunks[i].token_count)))
+      throw std::invalid_argument("gpu run: cache-tier chunk size disagrees with the model's KV layout");
+  const bool io_on = mode == RunMode::io_only || (mode == RunMode::cake && opt.io_enabled);
+  const bool compute_on = mode == RunMode::compute_only || (mode == RunMode::cake && opt.compute_enabled);
+  if (!io_on && !compute_on) throw std::invalid_argument("run: no side enabled");
+  const bool race = opt.race_to_finish && io_on && compute_on;
+  g.ensure_events(n);
+  check(cake_cuda_device_sync(), "pre-run sync");
+  long long launches0 = 0;
+  check(cake_model_launch_count(g.model, &launches0, 1), "launch count");
+
+  // ---------------------------------------------------------------- t = 0
+  RunTimer timer;
+  LiveRun run(g, plan, timer);
+  check(cake_event_record(g.ev_anchor->h, g.s_compute), "anchor");
+  run.t0 = timer.now_us();
+  check(cake_stream_wait_event(g.s_copy, g.ev_anchor->h), "order");
+  check(cake_memset_async(g.abort_flags.p, 0, g.n_pages * sizeof(std::int32_t), g.s_compute), "abort reset");
+  upload_tokens(g, tokens, g.s_compute);
+  GpuRunInfo info;
+  info.h2d_bytes = tokens.size() * sizeof(std::int32_t);
+
+  ClaimTable table(n);
+  GpuLoaderSink sink(run);
+  GpuPrefillBackend backend(run, opt.gpu->options().prior);
+  std::unique_ptr<TransferEngine> loader;
+  if (io_on) {
+    TransferOptions t;
+    t.throttle_quantum_bytes = opt.throttle_quantum_bytes;
+    t.jitter_max_us = opt.jitter_max_us;
+    t.jitter_seed = opt.jitter_seed;
+    t.record_slices = opt.record_slices;
+    t.sink = &sink;
+    if (race) {
+      t.contest = [&](const FetchTask& task, Micros io_eta) {
+        const auto c_eta = backend.expected_end_of(task.chunk.index);
+        return c_eta && io_eta + g.opt.race_margin_us < *c_eta;
+      };
+    }
+    loader = std::make_unique<TransferEngine>(store, trace, codec, &table, timer, std::move(t));
+    run.loader = loader.get();
+    std::vector<FetchTask> tasks;
+    tasks.reserve(n);
+    for (std::uint32_t i = n; i-- > 0;) tasks.push_back({plan.keys[i], plan.chunks[i], plan.encoded_bytes[i]});
+    loader->push_seq(std::move(tasks));
+  }
+
+  RunReport rep;
+  rep.mode = mode;
+  rep.n_chunks = n;
+  if (compute_on) {
+    ComputeEngine engine(cost, TokenBudget{opt.token_budget, power});
+    ComputeEngine::ForwardHooks hooks;
+    hooks.table = &table;
+    hooks.timer = &timer;
+    hooks.jitter_max_us = opt.jitter_max_us;
+    hooks.jitter_seed = opt.jitter_seed + 1;
+    hooks.backend = &backend;
+    if (loader) {
+      hooks.probe = &loader->resident_set();
+      hooks.signal_stop = [&loader] { loader->stop(); };
+    }
+    if (race) {
+      hooks.contest = [&](const ChunkSpec& c, Micros c_eta) {
+        const auto io_eta = loader->inflight_finish_estimate(c.index);
+        return io_eta && c_eta + g.opt.race_margin_us < *io_eta;
+      };
+    }
+    auto recs = engine.run_forward(plan.chunks, plan.keys, hooks);
+    rep.chunks.insert(rep.chunks.end(), recs.begin(), recs.end());
+  }
+  if (loader) {
+    loader->wait();
+    rep.chunks.insert(rep.chunks.end(), loader->records().begin(), loader->records().end());
+  }
+  detail::finalize_report(rep, 0);
+  rep.merge_point = merge_from_records(rep);
+  rep.computed_fraction = static_cast<double>(rep.merge_point) / n;
+
+  // ---------------------------------------------------------------- first token
+  const int rc = run.race_chunk.load();
+  const bool racer_won = rc >= 0 && ((run.racer.load() == kByCompute && run.commit[rc].load() == kByCompute) ||
+                                     (run.racer.load() == kByIo && run.commit[rc].load() == kByIo));
+  g.final_bt = racer_won ? g.bt_race.p : g.bt_primary.p;
+  check(cake_event_record(g.ev_copy_done->h, g.s_copy), "record");
+  check(cake_stream_wait_event(g.s_compute, g.ev_copy_done->h), "join streams");
+  const ChunkSpec& tail = plan.chunks[n - 1];
+  const bool tail_hidden = run.commit[n - 1].load() == kByCompute && backend.last_launched() == static_cast<int>(n - 1);
+  const long long T = static_cast<long long>(tail.token_start + tail.token_count);
+  check(cake_event_record(g.ev_final_start->h, g.s_compute), "record");
+  check(cake_final_logits(g.model, T, g.tokens.p + (T - 1), tail_hidden ? 0 : 1, static_cast<int>(tail.token_count) - 1,
+                          g.final_bt, g.logits.p, g.s_compute),
+        "final logits");
+  check(cake_d2h_async(g.h_logits.p, g.logits.p, g.cfg.vocab * sizeof(float), g.s_compute), "logits D2H");
+  check(cake_event_record(g.ev_logits->h, g.s_compute), "record");
+  check(cake_event_sync(g.ev_logits->h), "logits");
+  info.first_token_us = timer.now_us();
+  // ---------------------------------------------------------------- done
+
+  info.kv_resident_us = rep.ttft_us;
+  float ms = 0.f;
+  check(cake_event_elapsed_ms(g.ev_final_start->h, g.ev_logits->h, &ms), "elapsed");
+  info.final_step_us = static_cast<Micros>(std::llround(ms * 1000.0));
+  check(cake_event_elapsed_ms(g.ev_anchor->h, g.ev_logits->h, &ms), "elapsed");
+  info.device_ttft_ms = ms;
+  info.merge_point = rep.merge_point;
+  info.raced_chunk = rc;
+  info.race_winner = rc >= 0 ? (run.commit[rc].load() == kByCompute ? 0 : 1) : -1;
+  info.recomputed_last = !tail_hidden;
+  info.h2d_bytes += sink.h2d_bytes();
+  info.d2h_bytes = g.cfg.vocab * sizeof(float);
+  check(cake_model_launch_count(g.model, &info.kernel_launches, 0), "launch count");
+  info.logits.assign(g.h_logits.p, g.h_logits.p + g.cfg.vocab);
+  if (rc >= 0)
+    rep.events.push_back("race on chunk " + std::to_string(rc) + " won by " +
+                         (info.race_winner == 0 ? "compute" : "io"));
+  rep.events.push_back("first token at " + std::to_string(info.first_token_us) + "us");
+  g.last = std::move(info);
+  return rep;
+}
+
+}  // namespace detail
+
+}  // namespace cake
