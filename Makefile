@@ -2,7 +2,8 @@
 #   make            -> CUDA layer + host runtime + CPU oracle (+ reference build when present)
 #   make cuda host  -> individual pieces
 NVCC    ?= nvcc
-CXX     ?= g++
+# the system toolchain (an /opt/gcc wrapper on PATH/CXX produced miscompiled -O2 objects here)
+CXX     := $(firstword $(wildcard /usr/bin/g++) g++)
 CC      ?= gcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
 PKG     := paper_2410_03065_b200

@@ -54,8 +54,8 @@ CAKE_API int cake_kv_bytes_per_token(uint32_t n_layers, uint32_t hidden, uint32_
 CAKE_API int cake_split_into_chunks(uint64_t total_tokens, uint32_t chunk_size, uint32_t* n_out, uint64_t* starts,
                                     uint32_t* counts, uint32_t cap);
 /* reference proj/include/cake/scheduler.hpp:68-69 */
-CAKE_API int cake_oracle_best_split(const int64_t* compute_us, const int64_t* fetch_us, uint32_t n, uint32_t* k_star,
-                                    int64_t* ttft_star);
+CAKE_API int cake_oracle_best_split(const int64_t* compute_us, uint32_t n_compute, const int64_t* fetch_us,
+                                    uint32_t n_fetch, uint32_t* k_star, int64_t* ttft_star);
 
 /* ---- scheduler (reference proj/include/cake/scheduler.hpp:75-83) ---- */
 typedef struct cake_record {

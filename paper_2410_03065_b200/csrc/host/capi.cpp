@@ -180,10 +180,11 @@ int cake_split_into_chunks(uint64_t total_tokens, uint32_t chunk_size, uint32_t*
   });
 }
 
-int cake_oracle_best_split(const int64_t* compute_us, const int64_t* fetch_us, uint32_t n, uint32_t* k_star,
-                           int64_t* ttft_star) {
+int cake_oracle_best_split(const int64_t* compute_us, uint32_t n_compute, const int64_t* fetch_us, uint32_t n_fetch,
+                           uint32_t* k_star, int64_t* ttft_star) {
   return guarded([&] {
-    const SplitChoice s = oracle_best_split(std::span<const Micros>(compute_us, n), std::span<const Micros>(fetch_us, n));
+    const SplitChoice s = oracle_best_split(std::span<const Micros>(compute_us, n_compute),
+                                            std::span<const Micros>(fetch_us, n_fetch));
     *k_star = s.k_star;
     *ttft_star = s.ttft_star;
   });

@@ -3,6 +3,8 @@
 // run that replaces reference run_live (proj/src/scheduler.cpp:229-278).
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -338,6 +340,9 @@ struct LiveRun {
   std::atomic<int> race_chunk{-1};
   std::atomic<int> racer{-1};  // kByCompute / kByIo
   TransferEngine* loader = nullptr;
+  std::mutex commit_mu;
+  std::condition_variable commit_cv;
+  std::uint32_t n_committed = 0;
 
   LiveRun(GpuContext::Impl& g_, const RunPlan& p, const RunTimer& t) : g(g_), plan(p), timer(t) {
     commit = std::make_unique<std::atomic<int>[]>(p.chunks.size());
@@ -352,7 +357,24 @@ struct LiveRun {
 
   bool try_commit(std::uint32_t i, int who) {
     int expected = kNone;
-    return commit[i].compare_exchange_strong(expected, who);
+    if (!commit[i].compare_exchange_strong(expected, who)) return false;
+    {
+      std::lock_guard lk(commit_mu);
+      ++n_committed;
+    }
+    commit_cv.notify_all();
+    return true;
+  }
+
+  // Block until every chunk has a committed source (the first token only
+  // needs that), or the loader stopped without delivering (error path).
+  void wait_all_committed() {
+    const auto n = static_cast<std::uint32_t>(plan.chunks.size());
+    std::unique_lock lk(commit_mu);
+    while (n_committed < n) {
+      if (commit_cv.wait_for(lk, std::chrono::milliseconds(1), [&] { return n_committed >= n; })) break;
+      if (loader == nullptr || loader->idle()) break;
+    }
   }
 
   // Second page set for contested chunk k, uploaded on the racer's stream
@@ -597,21 +619,21 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
     auto recs = engine.run_forward(plan.chunks, plan.keys, hooks);
     rep.chunks.insert(rep.chunks.end(), recs.begin(), recs.end());
   }
-  if (loader) {
-    loader->wait();
-    rep.chunks.insert(rep.chunks.end(), loader->records().begin(), loader->records().end());
-  }
-  detail::finalize_report(rep, 0);
-  rep.merge_point = merge_from_records(rep);
-  rep.computed_fraction = static_cast<double>(rep.merge_point) / n;
+  // The first token needs every chunk committed, not the loader's threads
+  // drained (a pacer may still be winding down a chunk it lost).
+  run.wait_all_committed();
+  if (run.n_committed < n && loader) loader->wait();  // surfaces the loader's error, if any
+  if (run.n_committed < n) throw std::logic_error("run: chunk coverage is incomplete");
 
   // ---------------------------------------------------------------- first token
   const int rc = run.race_chunk.load();
   const bool racer_won = rc >= 0 && ((run.racer.load() == kByCompute && run.commit[rc].load() == kByCompute) ||
                                      (run.racer.load() == kByIo && run.commit[rc].load() == kByIo));
   g.final_bt = racer_won ? g.bt_race.p : g.bt_primary.p;
-  check(cake_event_record(g.ev_copy_done->h, g.s_copy), "record");
-  check(cake_stream_wait_event(g.s_compute, g.ev_copy_done->h), "join streams");
+  // No stream join needed: every io-committed chunk's scatter event has
+  // already completed (the commit happens after its event sync), and
+  // whatever the copy stream still carries (a lost race) writes pages the
+  // final block table does not reference.
   const ChunkSpec& tail = plan.chunks[n - 1];
   const bool tail_hidden = run.commit[n - 1].load() == kByCompute && backend.last_launched() == static_cast<int>(n - 1);
   const long long T = static_cast<long long>(tail.token_start + tail.token_count);
@@ -624,6 +646,13 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   check(cake_event_sync(g.ev_logits->h), "logits");
   info.first_token_us = timer.now_us();
   // ---------------------------------------------------------------- done
+  if (loader) {
+    loader->wait();
+    rep.chunks.insert(rep.chunks.end(), loader->records().begin(), loader->records().end());
+  }
+  detail::finalize_report(rep, 0);
+  rep.merge_point = merge_from_records(rep);
+  rep.computed_fraction = static_cast<double>(rep.merge_point) / n;
 
   info.kv_resident_us = rep.ttft_us;
   float ms = 0.f;
