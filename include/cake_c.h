@@ -176,6 +176,8 @@ CAKE_API int cake_gpu_logits(const cake_gpu* g, float* out, int n);
 CAKE_API int cake_gpu_read_chunk(const cake_gpu* g, uint64_t token_start, uint32_t token_count, uint8_t* out,
                                  uint64_t cap);
 CAKE_API int cake_gpu_kernel_stats(cake_gpu* g, cake_kernel_stat* out, int reset);
+/* Event-bracket kernel classes (bit CAKE_K_*; -1 all, 0 none) from now on. */
+CAKE_API int cake_gpu_set_profiling(cake_gpu* g, int mask);
 CAKE_API void* cake_gpu_model(cake_gpu* g); /* cake_model* for direct C-ABI CUDA calls */
 CAKE_API void* cake_gpu_compute_stream(cake_gpu* g);
 

@@ -178,9 +178,9 @@ typedef struct cake_kernel_stat {
   double flops;  /* algorithmic */
   double bytes;  /* algorithmic */
 } cake_kernel_stat;
-/* When enabled, every launch of a tracked kernel class is bracketed by CUDA
- * events on its stream; stats resolve (and reset) on read. */
-CAKE_API int cake_model_set_profiling(cake_model* m, int enabled);
+/* mask bit k (CAKE_K_*): every launch of kernel class k is bracketed by CUDA
+ * events on its stream (-1 = all, 0 = off); stats resolve (and reset) on read. */
+CAKE_API int cake_model_set_profiling(cake_model* m, int mask);
 CAKE_API int cake_model_kernel_stats(cake_model* m, cake_kernel_stat* out /* [CAKE_K_COUNT] */, int reset);
 CAKE_API int cake_model_launch_count(cake_model* m, long long* n, int reset);
 

@@ -19,6 +19,7 @@
 #include "cake_cuda.h"
 #include "elementwise.cuh"
 #include "gemm.cuh"
+#include "skinny.cuh"
 
 using namespace cake_dev;
 using bf16 = __nv_bfloat16;
@@ -195,7 +196,7 @@ struct cake_model {
   float* tp_buf = nullptr;  // fp32 partial sums for the TP all-reduce
   CUtensorMap a_xn, a_attn, a_act;
   ncclComm_t comm = nullptr;
-  bool profiling = false;
+  unsigned profile_mask = 0;  // bit k: bracket launches of kernel class k with events
   std::mutex prof_mu;  // launches come from the compute thread and the loader's pacer thread
   std::vector<ProfPair> prof;
   std::vector<cudaEvent_t> event_pool;
@@ -227,7 +228,7 @@ struct ProfScope {
       : m(m_), kind(kind_), s(s_), flops(f), bytes(b) {
     std::lock_guard<std::mutex> g(m->prof_mu);
     m->launches++;
-    if (m->profiling) {
+    if (m->profile_mask & (1u << kind)) {
       a = pool_event(m);
       cudaEventRecord(a, s);
     }
@@ -345,6 +346,96 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
       attn_combine_kernel<64><<<(rows + wpb - 1) / wpb, wpb * 32, 0, s>>>(m->part_o, m->part_lse, m->attn, rows, splits,
                                                                          abort_flag);
     CKL();
+  }
+  return CAKE_OK;
+}
+
+template <int EPI>
+int launch_skinny(cake_model* m, int kind, const SkinnyArgs& a, double rows, cudaStream_t s) {
+  auto kern = skinny_kernel<EPI>;
+  static bool cfgd = false;
+  if (!cfgd) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    cfgd = true;
+  }
+  const int smem = a.M * a.K * 2;
+  const int blocks = std::max(1, std::min((a.units + kSkinnyWarps - 1) / kSkinnyWarps, num_sms() * 16));
+  ProfScope ps(m, kind, s, 2.0 * a.M * rows * a.K, 2.0 * rows * a.K);
+  kern<<<blocks, kSkinnyWarps * 32, smem, s>>>(a);
+  CKL();
+  return CAKE_OK;
+}
+
+// Row-parallel skinny projection into the residual stream (TP: partials + all-reduce).
+int skinny_row_parallel(cake_model* m, int kind, const bf16* W, const bf16* x, int K, cudaStream_t s) {
+  SkinnyArgs a{};
+  a.W = W;
+  a.x = x;
+  a.M = 1;
+  a.K = K;
+  a.units = m->H;
+  if (m->cfg.tp_size == 1) {
+    a.resid = m->h;
+    a.ldr = m->H;
+    return launch_skinny<kSkResid>(m, kind, a, m->H, s);
+  }
+  if (!m->comm) return fail(CAKE_ESTATE, "tp_size > 1 but no NCCL communicator attached");
+  a.out = m->tp_buf;
+  a.ldo = m->H;
+  CKS(launch_skinny<kSkF32>(m, kind, a, m->H, s));
+  {
+    ProfScope ps(m, CAKE_K_ALLREDUCE, s, 0.0, 4.0 * m->H);
+    ncclResult_t r = ncclAllReduce(m->tp_buf, m->tp_buf, static_cast<size_t>(m->H), ncclFloat32, ncclSum, m->comm, s);
+    if (r != ncclSuccess) return fail(CAKE_ENCCL + r, "allreduce: %s", ncclGetErrorString(r));
+  }
+  add_inplace_kernel<<<1, 256, 0, s>>>(m->h, m->tp_buf, m->H, nullptr);
+  CKL();
+  return CAKE_OK;
+}
+
+int rmsnorm(cake_model* m, const bf16* gamma, long long row0, int rows, const int32_t* abort_flag, cudaStream_t s);
+
+// First-token step over a complete cache: the last prompt token (position
+// T-1) as a q-only pass, every projection a weight stream.
+int last_token_pass(cake_model* m, const int32_t* d_token, long long T, const int32_t* bt, cudaStream_t s) {
+  const int H = m->H;
+  {
+    ProfScope ps(m, CAKE_K_EMBED, s, 0.0, H * 6.0);
+    embed_kernel<<<1, 128, 0, s>>>(d_token, m->embed, m->h, H, nullptr);
+    CKL();
+  }
+  for (int l = 0; l < m->L; ++l) {
+    LayerWeights& lw = m->layers[l];
+    CKS(rmsnorm(m, lw.ln1, 0, 1, nullptr, s));
+    {
+      SkinnyArgs a{};
+      a.W = lw.wqkv;  // q rows come first
+      a.x = m->xn;
+      a.M = 1;
+      a.K = H;
+      a.units = m->nq * m->hd / 2;
+      a.q_out = m->q;
+      a.ldo = m->nq * m->hd;
+      a.rope = m->rope;
+      a.pos0 = T - 1;
+      a.head_dim = m->hd;
+      CKS(launch_skinny<kSkQRope>(m, CAKE_K_GEMM_QKV, a, m->nq * m->hd, s));
+    }
+    CKS(attention(m, T - 1, 1, l, bt, nullptr, s));
+    CKS(skinny_row_parallel(m, CAKE_K_GEMM_O, lw.wo, m->attn, m->nq * m->hd, s));
+    CKS(rmsnorm(m, lw.ln2, 0, 1, nullptr, s));
+    {
+      SkinnyArgs a{};
+      a.W = lw.wgu;
+      a.x = m->xn;
+      a.M = 1;
+      a.K = H;
+      a.units = m->F;
+      a.act = m->act;
+      a.ld_act = m->F;
+      CKS(launch_skinny<kSkSwiglu>(m, CAKE_K_GEMM_GU, a, 2.0 * m->F, s));
+    }
+    CKS(skinny_row_parallel(m, CAKE_K_GEMM_D, lw.wd, m->act, m->F, s));
   }
   return CAKE_OK;
 }
@@ -642,6 +733,9 @@ int cake_model_create(const cake_model_config* cfg, cake_model** out) {
   const size_t page_elems = static_cast<size_t>(m->L) * 2 * m->nkv * c.page_tokens * hd;
   m->pool_bytes = page_elems * sizeof(bf16) * m->n_phys_pages;
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->pool), m->pool_bytes))) return bail(st);
+  // zeroed once: keys past a chunk's end are masked (p = 0) but still read, so
+  // never-written pages must hold finite values
+  cudaMemset(m->pool, 0, m->pool_bytes);
 
   // ---- RoPE table: cos/sin(pos * theta^(-2i/hd)), computed in double.
   {
@@ -709,8 +803,9 @@ int cake_model_set_comm(cake_model* m, void* comm) {
   return CAKE_OK;
 }
 
-int cake_model_set_profiling(cake_model* m, int enabled) {
-  m->profiling = enabled != 0;
+int cake_model_set_profiling(cake_model* m, int mask) {
+  std::lock_guard<std::mutex> g(m->prof_mu);
+  m->profile_mask = static_cast<unsigned>(mask);
   return CAKE_OK;
 }
 
@@ -816,7 +911,7 @@ int cake_final_logits(cake_model* m, long long T, const int32_t* d_last_token, i
   cudaStream_t s = S(stream);
   int row = last_row;
   if (recompute) {
-    CKS(cake_prefill_chunk(m, d_last_token, T - 1, 1, d_block_table, nullptr, CAKE_PREFILL_NO_KV_WRITE, stream));
+    CKS(last_token_pass(m, d_last_token, T, d_block_table, s));
     row = 0;
   }
   if (row < 0 || row >= m->rows_cap) return fail(CAKE_EINVAL, "final: bad row");

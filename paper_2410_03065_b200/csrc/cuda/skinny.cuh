@@ -1,0 +1,127 @@
+// Weight-streaming projections for the first-token step (M <= 4 rows).
+//
+// With one query row a projection is a pure weight read (HBM-bound: 416 MB
+// per Llama-3-8B layer for q/o/gate-up/down). The tcgen05 tile kernel would
+// run it on N/BLOCK_N CTAs only (16..112), far below the SM count; here
+// every warp owns one output unit and streams its weight row(s) with 16-B
+// loads, so thousands of warps keep the HBM pipes full. The unit epilogues
+// mirror the tile kernel's: q rows pair (d, d + hd/2) for RoPE, gate/up rows
+// pair through the 128-row interleave, o/down rows add into the fp32
+// residual stream.
+#pragma once
+
+#include "ptx.cuh"
+
+namespace cake_dev {
+
+enum SkinnyEpi : int { kSkF32 = 0, kSkResid = 1, kSkQRope = 2, kSkSwiglu = 3 };
+
+struct SkinnyArgs {
+  const __nv_bfloat16* W;  // [rows, K]
+  const __nv_bfloat16* x;  // [M, K]
+  int M, K;
+  int units;               // output units (rows, or row pairs)
+  float* out;              // kSkF32: [M, rows]
+  int ldo;
+  float* resid;            // kSkResid: [M, ldr]
+  int ldr;
+  __nv_bfloat16* q_out;    // kSkQRope: [M, n_q * hd]
+  const float2* rope;      // [pos][hd/2]
+  long long pos0;
+  int head_dim;
+  __nv_bfloat16* act;      // kSkSwiglu: [M, F]
+  int ld_act;
+};
+
+constexpr int kSkinnyWarps = 8;
+
+template <int NR>
+__device__ __forceinline__ void skinny_dot(const __nv_bfloat16* const (&w)[NR], const __nv_bfloat16* xs, int M,
+                                           int K, float (&acc)[NR][4]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+#pragma unroll
+    for (int m = 0; m < 4; ++m) acc[r][m] = 0.f;
+#pragma unroll 2
+  for (int k = lane * 8; k < K; k += 256) {
+    uint4 wv[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) wv[r] = __ldg(reinterpret_cast<const uint4*>(w[r] + k));
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      if (m >= M) break;
+      const uint4 xv = *reinterpret_cast<const uint4*>(xs + static_cast<size_t>(m) * K + k);
+      const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&xv);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(&wv[r]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 a = __bfloat1622float2(wp[e]);
+          const float2 b = __bfloat1622float2(xp[e]);
+          acc[r][m] = fmaf(a.x, b.x, acc[r][m]);
+          acc[r][m] = fmaf(a.y, b.y, acc[r][m]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[r][m] += __shfl_xor_sync(0xffffffff, acc[r][m], o);
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kSkinnyWarps * 32) skinny_kernel(const SkinnyArgs a) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm);
+  const int total = a.M * a.K;
+  for (int i = threadIdx.x * 8; i < total; i += blockDim.x * 8)
+    *reinterpret_cast<uint4*>(xs + i) = *reinterpret_cast<const uint4*>(a.x + i);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int u = blockIdx.x * kSkinnyWarps + (threadIdx.x >> 5); u < a.units; u += gridDim.x * kSkinnyWarps) {
+    if constexpr (EPI == kSkF32 || EPI == kSkResid) {
+      const __nv_bfloat16* w[1] = {a.W + static_cast<size_t>(u) * a.K};
+      float acc[1][4];
+      skinny_dot<1>(w, xs, a.M, a.K, acc);
+      if (lane == 0)
+        for (int m = 0; m < a.M; ++m) {
+          if constexpr (EPI == kSkF32)
+            a.out[static_cast<size_t>(m) * a.ldo + u] = acc[0][m];
+          else
+            a.resid[static_cast<size_t>(m) * a.ldr + u] += acc[0][m];
+        }
+    } else if constexpr (EPI == kSkQRope) {
+      const int half = a.head_dim >> 1;
+      const int head = u / half, i = u % half;
+      const int r0 = head * a.head_dim + i;
+      const __nv_bfloat16* w[2] = {a.W + static_cast<size_t>(r0) * a.K, a.W + static_cast<size_t>(r0 + half) * a.K};
+      float acc[2][4];
+      skinny_dot<2>(w, xs, a.M, a.K, acc);
+      if (lane == 0)
+        for (int m = 0; m < a.M; ++m) {
+          const float2 cs = a.rope[(a.pos0 + m) * half + i];
+          const float x0 = acc[0][m], x1 = acc[1][m];
+          __nv_bfloat16* q = a.q_out + static_cast<size_t>(m) * a.ldo + r0;
+          q[0] = __float2bfloat16_rn(x0 * cs.x - x1 * cs.y);
+          q[half] = __float2bfloat16_rn(x1 * cs.x + x0 * cs.y);
+        }
+    } else if constexpr (EPI == kSkSwiglu) {
+      const int g = (u / 128) * 256 + (u % 128);
+      const __nv_bfloat16* w[2] = {a.W + static_cast<size_t>(g) * a.K, a.W + static_cast<size_t>(g + 128) * a.K};
+      float acc[2][4];
+      skinny_dot<2>(w, xs, a.M, a.K, acc);
+      if (lane == 0)
+        for (int m = 0; m < a.M; ++m) {
+          const float gt = acc[0][m];
+          a.act[static_cast<size_t>(m) * a.ld_act + u] = __float2bfloat16_rn(gt / (1.0f + __expf(-gt)) * acc[1][m]);
+        }
+    }
+  }
+}
+
+}  // namespace cake_dev

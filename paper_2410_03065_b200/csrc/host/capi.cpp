@@ -469,6 +469,12 @@ int cake_gpu_kernel_stats(cake_gpu* g, cake_kernel_stat* out, int reset) {
   });
 }
 
+int cake_gpu_set_profiling(cake_gpu* g, int mask) {
+  return guarded([&] {
+    if (cake_model_set_profiling(g->ctx->model(), mask) != CAKE_OK) throw std::runtime_error("set profiling failed");
+  });
+}
+
 void* cake_gpu_model(cake_gpu* g) { return g->ctx->model(); }
 void* cake_gpu_compute_stream(cake_gpu* g) { return g->ctx->compute_stream(); }
 #endif  // CAKE_REFERENCE_BUILD

@@ -162,7 +162,7 @@ GpuContext::GpuContext(const GpuModelConfig& cfg, const GpuOptions& opt) : impl_
     if (!opt.nccl_comm) throw std::invalid_argument("gpu: tp_size > 1 needs an NCCL communicator");
     check(cake_model_set_comm(g.model, opt.nccl_comm), "set comm");
   }
-  check(cake_model_set_profiling(g.model, opt.profile_kernels ? 1 : 0), "profiling");
+  check(cake_model_set_profiling(g.model, opt.profile_kernels ? -1 : 0), "profiling");
   check(cake_stream_create(&g.s_compute, 0), "stream");
   check(cake_stream_create(&g.s_copy, 1), "stream");     // loader work jumps the queue for free SMs
   check(cake_stream_create(&g.s_control, 1), "stream");
@@ -222,7 +222,11 @@ void check_chunking(const GpuContext::Impl& g, std::span<const ChunkSpec> chunks
 }
 
 void upload_tokens(GpuContext::Impl& g, const std::vector<std::uint32_t>& ids, void* stream) {
-  for (std::size_t i = 0; i < ids.size(); ++i) g.h_tokens.p[i] = static_cast<std::int32_t>(ids[i]);
+  for (std::size_t i = 0; i < ids.size(); ++i) {
+    if (ids[i] >= static_cast<std::uint32_t>(g.cfg.vocab))
+      throw std::invalid_argument("gpu: token id " + std::to_string(ids[i]) + " outside the vocabulary");
+    g.h_tokens.p[i] = static_cast<std::int32_t>(ids[i]);
+  }
   check(cake_h2d_async(g.tokens.p, g.h_tokens.p, ids.size() * sizeof(std::int32_t), stream), "tokens H2D");
 }
 

@@ -126,6 +126,16 @@ class GpuRuntime:
         self.n.call("cake_gpu_read_chunk", self.h, token_start, token_count, out, nbytes)
         return out.raw
 
+    def set_profiling(self, kernels="all"):
+        """Bracket launches of the named kernel classes with CUDA events ("all", None, or a list)."""
+        if kernels == "all":
+            mask = -1
+        elif not kernels:
+            mask = 0
+        else:
+            mask = sum(1 << N.KERNEL_NAMES.index(k) for k in kernels)
+        self.n.call("cake_gpu_set_profiling", self.h, mask)
+
     def kernel_stats(self, reset: bool = True) -> dict:
         arr = (N.CakeKernelStat * len(N.KERNEL_NAMES))()
         self.n.call("cake_gpu_kernel_stats", self.h, arr, 1 if reset else 0)

@@ -74,7 +74,7 @@ def tiny_rt():
         pytest.skip("no GPU")
     from paper_2410_03065_b200.runtime import GpuRuntime
 
-    return GpuRuntime((2, 256, 4, 2, 128, 1024, 1000), max_tokens=1024, max_chunk=256)
+    return GpuRuntime((2, 256, 4, 2, 128, 1024, 32000), max_tokens=1024, max_chunk=256)
 
 
 def test_kv_scatter_gather_bit_exact(cu, tiny_rt):

@@ -15,8 +15,8 @@ pytestmark = pytest.mark.gpu
 CONFIGS = {
     # name: (dims, T, chunk)
     "tiny": ((2, 256, 4, 4, 64, 1024, 32000), 2048, 256),
-    "gqa_hd64": ((2, 512, 8, 2, 64, 1024, 4096), 1024, 256),
-    "gqa_hd128": ((2, 1024, 8, 2, 128, 2048, 8192), 1024, 512),
+    "gqa_hd64": ((2, 512, 8, 2, 64, 1024, 32000), 1024, 256),
+    "gqa_hd128": ((2, 1024, 8, 2, 128, 2048, 32768), 1024, 512),
 }
 
 
