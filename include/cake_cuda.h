@@ -117,6 +117,10 @@ typedef struct cake_model cake_model;
 CAKE_API int cake_model_create(const cake_model_config* cfg, cake_model** out);
 CAKE_API int cake_model_destroy(cake_model* m);
 CAKE_API int cake_model_get_info(const cake_model* m, cake_model_info* out);
+/* Attention kernel variant: 0 = tcgen05/TMEM flash attention (default, the
+ * product path), 1 = mma.sync flash attention (kept as an independent
+ * cross-check in tests/test_gpu_kernels.py). */
+CAKE_API int cake_model_set_attention_impl(cake_model* m, int impl);
 /* Attach an NCCL communicator (ncclComm_t) for tp_size > 1. */
 CAKE_API int cake_model_set_comm(cake_model* m, void* nccl_comm);
 

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "attention.cuh"
+#include "attention_tc.cuh"
 #include "cake_cuda.h"
 #include "elementwise.cuh"
 #include "gemm.cuh"
@@ -89,6 +90,21 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uin
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CAKE_EINVAL, "tensor map encode failed (%d) rows=%llu cols=%llu", (int)r,
                                      (unsigned long long)rows, (unsigned long long)cols);
+  return CAKE_OK;
+}
+
+// bf16 3-D tensor [d2][d1][d0] (d0 contiguous), SW128, box (64, b1, b2).
+int make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b1, uint32_t b2) {
+  auto fn = encode_fn();
+  if (!fn) return fail(CAKE_ESTATE, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
+  cuuint32_t box[3] = {64, b1, b2};
+  cuuint32_t elem[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, elem,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CAKE_EINVAL, "3-D tensor map encode failed (%d)", (int)r);
   return CAKE_OK;
 }
 
@@ -195,6 +211,8 @@ struct cake_model {
   size_t part_rows_cap = 0;  // splits * chunk rows * local q heads the partials hold
   float* tp_buf = nullptr;  // fp32 partial sums for the TP all-reduce
   CUtensorMap a_xn, a_attn, a_act;
+  CUtensorMap tm_q, tm_kv;  // attention: Q rows of a GQA group, paged K/V pool
+  int attn_impl = 0;        // 0 tcgen05 (product), 1 mma.sync (cross-check)
   ncclComm_t comm = nullptr;
   unsigned profile_mask = 0;  // bit k: bracket launches of kernel class k with events
   std::mutex prof_mu;  // launches come from the compute thread and the loader's pacer thread
@@ -289,14 +307,70 @@ namespace {
 int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, const int32_t* bt,
               const int32_t* abort_flag, cudaStream_t s) {
   const int G = m->nq / m->nkv;
-  const int tok_per_tile = kAttnRows / G;
+  const bool tc = m->attn_impl == 0;
+  const int rows_per_cta = tc ? kFaRows : kAttnRows;
+  const int tok_per_tile = rows_per_cta / G;
   const int qtiles = (chunk_len + tok_per_tile - 1) / tok_per_tile;
   const long long kv_end = chunk_start + chunk_len;
   const int n_pages = static_cast<int>((kv_end + kAttnPage - 1) / kAttnPage);
   const int base_ctas = qtiles * m->nkv;
-  const int target = 2 * num_sms();
   const int cap = static_cast<int>(m->part_rows_cap / (static_cast<size_t>(chunk_len) * m->nq));
-  int splits = std::max(1, std::min({(target + base_ctas - 1) / base_ctas, std::max(1, n_pages / 4), m->max_splits, cap}));
+  int splits = 1;
+  if (tc) {
+    // one CTA per SM: pick the split count with the fullest last wave, >= 8 pages per split
+    const int max_s = std::max(1, std::min({n_pages / 8, m->max_splits, cap}));
+    double best = 0.0;
+    for (int sp = 1; sp <= max_s; ++sp) {
+      const int ctas = base_ctas * sp;
+      const int waves = (ctas + num_sms() - 1) / num_sms();
+      const double eff = static_cast<double>(ctas) / (static_cast<double>(waves) * num_sms());
+      if (eff > best + 0.02) {
+        best = eff;
+        splits = sp;
+      }
+    }
+  } else {
+    const int target = 2 * num_sms();
+    splits = std::max(1, std::min({(target + base_ctas - 1) / base_ctas, std::max(1, n_pages / 4), m->max_splits, cap}));
+  }
+  // algorithmic work: 4 * hd * (visible keys) per (query, head)
+  const double vis = static_cast<double>(chunk_len) * chunk_start + 0.5 * chunk_len * (chunk_len + 1.0);
+  const double flops = 4.0 * m->hd * m->nq * vis;
+  const double bytes = static_cast<double>(kv_end) * m->nkv * m->hd * 2 * 2 + 2.0 * chunk_len * m->nq * m->hd * 2;
+  ProfScope ps(m, CAKE_K_ATTN, s, flops, bytes);
+  dim3 grid(qtiles, m->nkv, splits);
+  if (tc) {
+    FaArgs fa;
+    fa.block_table = bt;
+    fa.out = m->attn;
+    fa.part_o = m->part_o;
+    fa.part_lse = m->part_lse;
+    fa.chunk_start = chunk_start;
+    fa.chunk_len = chunk_len;
+    fa.n_q_heads = m->nq;
+    fa.n_kv_heads = m->nkv;
+    fa.layer = layer;
+    fa.n_layers = m->L;
+    fa.num_splits = splits;
+    fa.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(m->hd));
+    fa.abort_flag = abort_flag;
+    if (m->hd == 128) {
+      static bool cfgd = false;
+      if (!cfgd) {
+        CK(cudaFuncSetAttribute(attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, FaCfg<128>::kSmem));
+        cfgd = true;
+      }
+      attn_tc_kernel<128><<<grid, kFaThreads, FaCfg<128>::kSmem, s>>>(m->tm_q, m->tm_kv, fa);
+    } else {
+      static bool cfgd = false;
+      if (!cfgd) {
+        CK(cudaFuncSetAttribute(attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, FaCfg<64>::kSmem));
+        cfgd = true;
+      }
+      attn_tc_kernel<64><<<grid, kFaThreads, FaCfg<64>::kSmem, s>>>(m->tm_q, m->tm_kv, fa);
+    }
+    CKL();
+  } else {
   AttnArgs a;
   a.q = m->q;
   a.pool = m->pool;
@@ -313,12 +387,6 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
   a.num_splits = splits;
   a.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(m->hd));
   a.abort_flag = abort_flag;
-  // algorithmic work: 4 * hd * (visible keys) per (query, head)
-  const double vis = static_cast<double>(chunk_len) * chunk_start + 0.5 * chunk_len * (chunk_len + 1.0);
-  const double flops = 4.0 * m->hd * m->nq * vis;
-  const double bytes = static_cast<double>(kv_end) * m->nkv * m->hd * 2 * 2 + 2.0 * chunk_len * m->nq * m->hd * 2;
-  ProfScope ps(m, CAKE_K_ATTN, s, flops, bytes);
-  dim3 grid(qtiles, m->nkv, splits);
   const int smem = (kAttnRows + 4 * kAttnPage) * m->hd * 2;
   if (m->hd == 128) {
     static bool cfgd = false;
@@ -336,6 +404,7 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
     attn_prefill_kernel<64><<<grid, kAttnThreads, smem, s>>>(a);
   }
   CKL();
+  }
   if (splits > 1) {
     const int rows = chunk_len * m->nq;
     const int wpb = 8;
@@ -775,6 +844,12 @@ int cake_model_create(const cake_model_config* cfg, cake_model** out) {
   if ((st = make_map(&m->a_xn, m->xn, R, H, 128))) return bail(st);
   if ((st = make_map(&m->a_attn, m->attn, R, m->nq * hd, 128))) return bail(st);
   if ((st = make_map(&m->a_act, m->act, R, F, 128))) return bail(st);
+  {
+    const int G = m->nq / m->nkv;
+    if ((st = make_map_3d(&m->tm_q, m->q, hd, m->nq, R, G, kFaRows / G))) return bail(st);
+    const uint64_t pool_rows = static_cast<uint64_t>(m->n_phys_pages) * m->L * 2 * m->nkv * c.page_tokens;
+    if ((st = make_map(&m->tm_kv, m->pool, pool_rows, hd, 64))) return bail(st);
+  }
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return bail(fail(CAKE_ECUDA + e, "model init: %s", cudaGetErrorString(e)));
   *out = m;
@@ -795,6 +870,12 @@ int cake_model_get_info(const cake_model* m, cake_model_info* o) {
   o->flops_per_token_linear =
       2LL * m->L * (static_cast<long long>(m->qkv_rows) * H + H * m->nq * m->hd + 2LL * m->F * H + H * m->F);
   o->kv_pool = m->pool;
+  return CAKE_OK;
+}
+
+int cake_model_set_attention_impl(cake_model* m, int impl) {
+  if (impl != 0 && impl != 1) return fail(CAKE_EINVAL, "attention impl must be 0 (tcgen05) or 1 (mma.sync)");
+  m->attn_impl = impl;
   return CAKE_OK;
 }
 

@@ -475,6 +475,12 @@ int cake_gpu_set_profiling(cake_gpu* g, int mask) {
   });
 }
 
+int cake_gpu_set_attention_impl(cake_gpu* g, int impl) {
+  return guarded([&] {
+    if (cake_model_set_attention_impl(g->ctx->model(), impl) != CAKE_OK) throw std::invalid_argument("bad impl");
+  });
+}
+
 void* cake_gpu_model(cake_gpu* g) { return g->ctx->model(); }
 void* cake_gpu_compute_stream(cake_gpu* g) { return g->ctx->compute_stream(); }
 #endif  // CAKE_REFERENCE_BUILD

@@ -126,6 +126,10 @@ class GpuRuntime:
         self.n.call("cake_gpu_read_chunk", self.h, token_start, token_count, out, nbytes)
         return out.raw
 
+    def set_attention_impl(self, impl: str):
+        """"tcgen05" (product path) or "mma_sync" (independent cross-check kernel)."""
+        self.n.call("cake_gpu_set_attention_impl", self.h, {"tcgen05": 0, "mma_sync": 1}[impl])
+
     def set_profiling(self, kernels="all"):
         """Bracket launches of the named kernel classes with CUDA events ("all", None, or a list)."""
         if kernels == "all":

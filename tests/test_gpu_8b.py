@@ -14,6 +14,11 @@ pytestmark = pytest.mark.gpu
 DIMS = (32, 4096, 32, 8, 128, 14336, 128256)
 
 
+def top1_ok(got, want, tol=2e-2):
+    """GPU arg-max is the oracle's arg-max, or a near-tie within the stated tolerance."""
+    return want[int(got.argmax())] >= want.max() - tol * np.abs(want).max()
+
+
 def rel(a, b):
     return float(np.abs(a - b).max() / (np.abs(b).max() + 1e-12))
 
@@ -42,14 +47,14 @@ def test_8b_two_layers_vs_oracle(gpu):
     want = ref.final_logits(C - 1)
     rt.run(tier, T, C, seed, mbps=64000, mode="compute_only")
     lg = rt.logits()
-    assert rel(lg, want) <= 2e-2 and int(lg.argmax()) == int(want.argmax())
+    assert rel(lg, want) <= 2e-2 and top1_ok(lg, want)
     kv = ref.kv()
     for s in range(0, T, C):
         got = llama_oracle.bf16_to_f32(np.frombuffer(rt.read_chunk(s, C), dtype=np.uint16)).reshape(2, 2, 8, C, 128)
         assert rel(got, kv[:, :, :, s:s + C, :]) <= 2e-2
     rt.run(tier, T, C, seed, mbps=64000, mode="io_only")  # loaded tail -> recomputed last token
     lg2 = rt.logits()
-    assert rel(lg2, want) <= 2e-2 and int(lg2.argmax()) == int(want.argmax())
+    assert rel(lg2, want) <= 2e-2 and top1_ok(lg2, want)
 
 
 def test_8b_full_32k_properties(gpu):

@@ -20,6 +20,11 @@ CONFIGS = {
 }
 
 
+def top1_ok(got, want, tol=2e-2):
+    """GPU arg-max is the oracle's arg-max, or a near-tie within the stated tolerance."""
+    return want[int(got.argmax())] >= want.max() - tol * np.abs(want).max()
+
+
 def rel(a, b):
     return float(np.abs(a - b).max() / (np.abs(b).max() + 1e-12))
 
@@ -77,7 +82,7 @@ def test_first_token_logits_match_oracle(setup, mode):
     assert r.recomputed_last == (mode == "io_only")
     assert rel(lg, want) <= 2e-2
     assert cos(lg, want) >= 0.999
-    assert int(lg.argmax()) == int(want.argmax())
+    assert top1_ok(lg, want)
 
 
 def test_loaded_kv_bit_exact(setup):
@@ -105,5 +110,21 @@ def test_assembled_cache_independent_of_merge_point(setup, mbps):
     for i, s in enumerate(range(0, T, C)):
         assert rt.read_chunk(s, C) == base[i], (mbps, i, r.merge_point)
     lg = rt.logits()
-    assert int(lg.argmax()) == int(setup["ref_logits"].argmax())
+    assert top1_ok(lg, setup["ref_logits"])
     assert rel(lg, setup["ref_logits"]) <= 2e-2
+
+
+def test_tcgen05_attention_matches_mma_sync_kernel(setup):
+    """The two independent attention kernels agree on the whole computed cache
+    (bf16 P in both; only accumulation order differs)."""
+    rt, T, C = setup["rt"], setup["T"], setup["C"]
+    rt.set_attention_impl("mma_sync")
+    rt.run(setup["tier"], T, C, 42, mbps=1000, mode="compute_only")
+    mma = [_chunk_kv(rt, s, C) for s in range(0, T, C)]
+    lg_mma = rt.logits()
+    rt.set_attention_impl("tcgen05")
+    rt.run(setup["tier"], T, C, 42, mbps=1000, mode="compute_only")
+    tc = [_chunk_kv(rt, s, C) for s in range(0, T, C)]
+    for a, b in zip(tc, mma):
+        assert rel(a, b) <= 2e-2
+    assert rel(rt.logits(), lg_mma) <= 2e-2
