@@ -119,6 +119,31 @@ int num_sms() {
   return g_num_sms;
 }
 
+// Stream-K scratch shared by every GEMM launch of the process (launches are
+// stream-ordered on one compute stream per device; the epoch keeps flags of
+// consecutive launches apart without a reset).
+struct StreamKScratch {
+  float* ws = nullptr;
+  int* flags = nullptr;
+  int epoch = 0;
+  std::mutex mu;
+};
+StreamKScratch g_sk;
+
+int streamk_scratch(float** ws, int** flags, int* epoch) {
+  std::lock_guard<std::mutex> lk(g_sk.mu);
+  if (!g_sk.ws) {
+    const size_t slots = static_cast<size_t>(num_sms());
+    CK(cudaMalloc(&g_sk.ws, slots * kGemmBlockM * 256 * sizeof(float)));
+    CK(cudaMalloc(&g_sk.flags, slots * sizeof(int)));
+    CK(cudaMemset(g_sk.flags, 0, slots * sizeof(int)));
+  }
+  *ws = g_sk.ws;
+  *flags = g_sk.flags;
+  *epoch = ++g_sk.epoch;
+  return CAKE_OK;
+}
+
 template <int BN, int EPI>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaStream_t s) {
   using Cfg = GemmCfg<BN>;
@@ -131,8 +156,10 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaSt
   a.num_m_blocks = (a.M + kGemmBlockM - 1) / kGemmBlockM;
   a.num_n_blocks = a.N / BN;
   a.num_k_blocks = a.K / kGemmBlockK;
-  const int tiles = a.num_m_blocks * a.num_n_blocks;
-  const int grid = std::min(tiles, num_sms());
+  const long long units = static_cast<long long>(a.num_m_blocks) * a.num_n_blocks * a.num_k_blocks;
+  // every CTA gets >= 8 k-blocks (and >= 1 unit, so no CTA is empty)
+  const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(num_sms(), units / 8)));
+  CKS(streamk_scratch(&a.sk_ws, &a.sk_flags, &a.epoch));
   kern<<<grid, kGemmThreads, Cfg::kSmemBytes, s>>>(ta, tb, a);
   CKL();
   return CAKE_OK;
@@ -511,7 +538,8 @@ int last_token_pass(cake_model* m, const int32_t* d_token, long long T, const in
 
 int rmsnorm(cake_model* m, const bf16* gamma, long long row0, int rows, const int32_t* abort_flag, cudaStream_t s) {
   ProfScope ps(m, CAKE_K_RMSNORM, s, 0.0, static_cast<double>(rows) * m->H * 6);
-  rmsnorm_kernel<<<rows, 256, 0, s>>>(m->h, gamma, m->xn, m->H, m->cfg.rms_eps, row0, abort_flag);
+  rmsnorm_kernel<<<(rows + kNormRowsPerCta - 1) / kNormRowsPerCta, kNormThreadsPerRow * kNormRowsPerCta, 0, s>>>(
+      m->h, gamma, m->xn, m->H, m->cfg.rms_eps, row0, rows, abort_flag);
   CKL();
   return CAKE_OK;
 }
@@ -710,7 +738,7 @@ int cake_model_create(const cake_model_config* cfg, cake_model** out) {
   if (c.n_heads % c.n_kv_heads || c.n_kv_heads % c.tp_size || c.n_heads % c.tp_size)
     return fail(CAKE_EINVAL, "model: heads must divide evenly (GQA groups, TP shards)");
   if (c.ffn % (128 * c.tp_size)) return fail(CAKE_EINVAL, "model: ffn / tp must be a multiple of 128");
-  if (c.hidden % 128) return fail(CAKE_EINVAL, "model: hidden must be a multiple of 128");
+  if (c.hidden % 128 || c.hidden > 8192) return fail(CAKE_EINVAL, "model: hidden must be a multiple of 128, <= 8192");
   if (c.max_chunk < 1 || c.max_tokens < 1) return fail(CAKE_EINVAL, "model: bad capacity");
   const int G = c.n_heads / c.n_kv_heads;
   if (kAttnRows % G) return fail(CAKE_EINVAL, "model: GQA group must divide %d", kAttnRows);
@@ -998,7 +1026,8 @@ int cake_final_logits(cake_model* m, long long T, const int32_t* d_last_token, i
   if (row < 0 || row >= m->rows_cap) return fail(CAKE_EINVAL, "final: bad row");
   {
     ProfScope ps(m, CAKE_K_RMSNORM, s, 0.0, m->H * 6.0);
-    rmsnorm_kernel<<<1, 256, 0, s>>>(m->h, m->final_norm, m->xn, m->H, m->cfg.rms_eps, row, nullptr);
+    rmsnorm_kernel<<<1, kNormThreadsPerRow * kNormRowsPerCta, 0, s>>>(m->h, m->final_norm, m->xn, m->H,
+                                                                       m->cfg.rms_eps, row, 1, nullptr);
     CKL();
   }
   {

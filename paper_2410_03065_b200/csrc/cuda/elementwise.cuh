@@ -82,38 +82,58 @@ __global__ void embed_kernel(const int* __restrict__ tokens, const __nv_bfloat16
 }
 
 // ------------------------------------------------------------ RMSNorm
-// y[m, :] = bf16( h[m, :] * rsqrt(mean(h^2) + eps) * gamma ). One CTA (256
-// threads) per row; fixed-order reduction (thread-strided partials, shuffle
-// tree, then warps in index order) so results are run-to-run identical.
-__global__ void rmsnorm_kernel(const float* __restrict__ h, const __nv_bfloat16* __restrict__ gamma,
-                               __nv_bfloat16* __restrict__ y, int hidden, float eps, long long row0,
-                               const int* abort_flag) {
+// y[m, :] = bf16( h[m, :] * rsqrt(mean(h^2) + eps) * gamma ).
+// 128 threads per row, 2 rows per CTA; a thread holds its (<= 16) float4 of
+// the row in registers, so the row is read once with all loads in flight.
+// Fixed-order reduction (per-thread sequential, shuffle tree, 4 warps in
+// index order): bit-identical run to run.
+constexpr int kNormThreadsPerRow = 128;
+constexpr int kNormRowsPerCta = 2;
+constexpr int kNormMaxVec = 16;  // hidden <= 128 * 16 * 4 = 8192
+
+__global__ void __launch_bounds__(kNormThreadsPerRow* kNormRowsPerCta)
+    rmsnorm_kernel(const float* __restrict__ h, const __nv_bfloat16* __restrict__ gamma,
+                   __nv_bfloat16* __restrict__ y, int hidden, float eps, long long row0, int rows,
+                   const int* abort_flag) {
   if (abort_flag != nullptr && *(volatile const int*)abort_flag) return;
-  __shared__ float warp_sums[32];
-  const long long m = row0 + blockIdx.x;
-  const float* x = h + m * hidden;
+  __shared__ float red[kNormRowsPerCta][kNormThreadsPerRow / 32];
+  const int sub = threadIdx.x / kNormThreadsPerRow;
+  const int tid = threadIdx.x % kNormThreadsPerRow;
+  const int r = blockIdx.x * kNormRowsPerCta + sub;
+  const bool live = r < rows;
+  const float4* x = reinterpret_cast<const float4*>(h + (row0 + (live ? r : 0)) * hidden);
+  const int nvec = hidden / 4;
+  float4 v[kNormMaxVec];
   float ss = 0.f;
-  for (int i = threadIdx.x * 4; i < hidden; i += blockDim.x * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(x + i);
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int i = 0; i < kNormMaxVec; ++i) {
+    const int idx = tid + i * kNormThreadsPerRow;
+    v[i] = (live && idx < nvec) ? x[idx] : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 #pragma unroll
+  for (int i = 0; i < kNormMaxVec; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+#pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
-  if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = ss;
+  if ((tid & 31) == 0) red[sub][tid >> 5] = ss;
   __syncthreads();
   float total = 0.f;
-  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) total += warp_sums[w];
-  const float r = rsqrtf(total / static_cast<float>(hidden) + eps);
-  __nv_bfloat16* out = y + static_cast<long long>(blockIdx.x) * hidden;
-  for (int i = threadIdx.x * 4; i < hidden; i += blockDim.x * 4) {
-    const float4 v = *reinterpret_cast<const float4*>(x + i);
-    const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162*>(gamma + i);
-    const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162*>(gamma + i + 2);
-    const float2 ga = __bfloat1622float2(g01), gb = __bfloat1622float2(g23);
+#pragma unroll
+  for (int w = 0; w < kNormThreadsPerRow / 32; ++w) total += red[sub][w];
+  if (!live) return;
+  const float rr = rsqrtf(total / static_cast<float>(hidden) + eps);
+  uint2* out = reinterpret_cast<uint2*>(y + static_cast<long long>(r) * hidden);
+  const uint2* g2 = reinterpret_cast<const uint2*>(gamma);
+#pragma unroll
+  for (int i = 0; i < kNormMaxVec; ++i) {
+    const int idx = tid + i * kNormThreadsPerRow;
+    if (idx >= nvec) break;
+    const uint2 gg = g2[idx];
+    const float2 ga = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gg.x));
+    const float2 gb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gg.y));
     uint2 o;
-    o.x = pack_bf16(v.x * r * ga.x, v.y * r * ga.y);
-    o.y = pack_bf16(v.z * r * gb.x, v.w * r * gb.y);
-    *reinterpret_cast<uint2*>(out + i) = o;
+    o.x = pack_bf16(v[i].x * rr * ga.x, v[i].y * rr * ga.y);
+    o.y = pack_bf16(v[i].z * rr * gb.x, v[i].w * rr * gb.y);
+    out[idx] = o;
   }
 }
 

@@ -1,16 +1,26 @@
-// Persistent warp-specialised tcgen05 GEMM for the chunk projections.
+// Persistent warp-specialised stream-K tcgen05 GEMM for the chunk projections.
 //
 //   C[M, N] = A[M, K] · B[N, K]^T     (both operands K-major bf16, fp32 accumulate in TMEM)
 //
 // A is the chunk's activations (M = chunk tokens), B a weight matrix stored
-// [out_features, in_features]. One CTA per SM walks tiles m-fastest so the
-// CTAs that share a weight tile run together and the weight is read from HBM
-// once per chunk. Roles (192 threads):
+// [out_features, in_features]. The work is the list of (tile, k-block) units,
+// tiles ordered m-fastest so CTAs that share a weight tile run together and
+// the weight is read from HBM once per chunk. Each of the grid's CTAs (one
+// per SM) takes an equal, contiguous run of units ("stream-K"): with M = 512
+// the per-projection tile counts (96 / 128 / 448) are not multiples of 148,
+// and whole-tile scheduling leaves up to a third of the SMs idle in the last
+// wave. A tile split across CTAs is reduced deterministically: a CTA's first
+// segment, if it starts inside a tile, is a partial (written to that CTA's
+// fp32 workspace slot, then flagged); the CTA that holds the tile's k = 0
+// segment (processed last by it) waits for those flags and adds the partials
+// in k order before the fused epilogue.
+//
+// Roles (192 threads):
 //   warp 0      TMA producer: A/B k-blocks into a kStages smem ring (SW128)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..5  epilogue: tcgen05.ld -> fused op -> global
-// Accumulators are double-buffered in TMEM so tile t's epilogue overlaps
-// tile t+1's MMAs.
+//   warps 2..5  epilogue: tcgen05.ld -> (+partials) -> fused op -> global
+// Accumulators are double-buffered in TMEM so segment s's epilogue overlaps
+// segment s+1's MMAs.
 //
 // Fused epilogues (the ops that follow each projection in a Llama block):
 //   kEpiBf16    plain bf16 store (tests / generic)
@@ -42,6 +52,10 @@ struct GemmArgs {
   long long pos0;           // absolute position of row 0
   int n_q_heads, n_kv_heads, head_dim, page_tokens, layer, n_layers;
   const int* abort_flag;    // optional: non-zero => skip (lost race / cancelled chunk)
+  // stream-K
+  float* sk_ws;             // [gridDim.x][128][BLOCK_N] partial tiles
+  int* sk_flags;            // [gridDim.x] = epoch when the CTA's partial is published
+  int epoch;
 };
 
 constexpr int kGemmBlockM = 128;
@@ -59,6 +73,27 @@ struct GemmCfg {
 };
 
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
+
+// Contiguous unit range of one CTA and its walk over (tile, [kb0, kb1)) segments.
+struct StreamK {
+  long long total, u, u_end;
+  int nk, grid;
+  __device__ StreamK(long long units, int num_k, int cta, int g) : total(units), nk(num_k), grid(g) {
+    u = units * cta / g;
+    u_end = units * (cta + 1) / g;
+  }
+  // CTA that owns unit v under the balanced split
+  __device__ int cta_of(long long v) const { return static_cast<int>(((v + 1) * grid + total - 1) / total - 1); }
+  __device__ bool next(int& tile, int& kb0, int& kb1) {
+    if (u >= u_end) return false;
+    tile = static_cast<int>(u / nk);
+    kb0 = static_cast<int>(u - static_cast<long long>(tile) * nk);
+    const long long rest = u_end - u;
+    kb1 = static_cast<int>(rest < static_cast<long long>(nk - kb0) ? kb0 + rest : nk);
+    u += kb1 - kb0;
+    return true;
+  }
+};
 
 template <int BLOCK_N, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -106,19 +141,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_tiles = args.num_m_blocks * args.num_n_blocks;
   const int nk = args.num_k_blocks;
+  const long long units = static_cast<long long>(args.num_m_blocks) * args.num_n_blocks * nk;
+  int tile, kb0, kb1;
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       const uint64_t pol_w = policy_evict_last();   // weights: reused by the other m-blocks
+      StreamK sk(units, nk, blockIdx.x, gridDim.x);
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      while (sk.next(tile, kb0, kb1)) {
         const int m_blk = tile % args.num_m_blocks;
         const int n_blk = tile / args.num_m_blocks;
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
           tma_load_2d(smem_a + stage * Cfg::kABytes, &tmap_a, &full_bar[stage], kb * kGemmBlockK,
@@ -136,15 +173,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       // ------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = umma_idesc_bf16(kGemmBlockM, BLOCK_N);
+      StreamK sk(units, nk, blockIdx.x, gridDim.x);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      while (sk.next(tile, kb0, kb1)) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BLOCK_N);
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem_a + stage * Cfg::kABytes);
@@ -152,7 +190,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int k = 0; k < kGemmBlockK / 16; ++k) {
             umma_bf16_ss(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32),
-                         idesc, (kb | k) != 0 ? 1u : 0u);
+                         idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty_bar[stage]);
           if (++stage == kStages) {
@@ -171,9 +209,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ------------------------------------------------ epilogue (warps 2..5)
     const int ew = warp & 3;  // TMEM lane quarter this warp may access
     const int row = ew * 32 + static_cast<int>(lane);
+    const int ep_tid = threadIdx.x - 64;  // 0..127
+    StreamK sk(units, nk, blockIdx.x, gridDim.x);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    while (sk.next(tile, kb0, kb1)) {
       const int m_blk = tile % args.num_m_blocks;
       const int n_blk = tile / args.num_m_blocks;
       const int m = m_blk * kGemmBlockM + row;
@@ -183,127 +223,173 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t tbase =
           tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * BLOCK_N);
 
-      if constexpr (EPI == kEpiBf16 || EPI == kEpiF32 || EPI == kEpiResid) {
+      if (kb0 > 0) {
+        // ---- partial segment: publish the fp32 tile in this CTA's slot
+        float4* slot = reinterpret_cast<float4*>(args.sk_ws + (static_cast<size_t>(blockIdx.x) * kGemmBlockM + row) * BLOCK_N);
 #pragma unroll 1
         for (int c = 0; c < BLOCK_N / 32; ++c) {
           uint32_t r[32];
           tmem_ld32(tbase + c * 32, r);
           tmem_ld_wait();
-          const int n0 = n_blk * BLOCK_N + c * 32;
-          if (valid && n0 < args.N) {
-            if constexpr (EPI == kEpiBf16) {
-              __nv_bfloat16* dst =
-                  reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<size_t>(m) * args.ldo + n0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            slot[c * 8 + q] = make_float4(__uint_as_float(r[q * 4]), __uint_as_float(r[q * 4 + 1]),
+                                          __uint_as_float(r[q * 4 + 2]), __uint_as_float(r[q * 4 + 3]));
+        }
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (ep_tid == 0) atomicExch(args.sk_flags + blockIdx.x, args.epoch);
+      } else {
+        // ---- full tile, or the k = 0 owner of a split tile: wait for the other parts
+        const long long u_tile = static_cast<long long>(tile) * nk;
+        const int first_part = sk.cta_of(u_tile) + 1;
+        const int last_part = kb1 < nk ? sk.cta_of(u_tile + nk - 1) : first_part - 1;
+        if (last_part >= first_part) {
+          if (ep_tid == 0) {
+            for (int p = first_part; p <= last_part; ++p)
+              while (*(volatile int*)(args.sk_flags + p) != args.epoch) __nanosleep(64);
+            __threadfence();
+          }
+          named_bar_sync(1, 128);
+        }
+        // accumulator chunk c (32 columns) of this thread's row, partials added in k order
+        auto load_acc = [&](int col, uint32_t (&r)[32]) {
+          tmem_ld32(tbase + col, r);
+          tmem_ld_wait();
+          for (int p = first_part; p <= last_part; ++p) {
+            const float4* part =
+                reinterpret_cast<const float4*>(args.sk_ws + (static_cast<size_t>(p) * kGemmBlockM + row) * BLOCK_N + col);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 v = __ldcg(part + q);
+              r[q * 4] = __float_as_uint(__uint_as_float(r[q * 4]) + v.x);
+              r[q * 4 + 1] = __float_as_uint(__uint_as_float(r[q * 4 + 1]) + v.y);
+              r[q * 4 + 2] = __float_as_uint(__uint_as_float(r[q * 4 + 2]) + v.z);
+              r[q * 4 + 3] = __float_as_uint(__uint_as_float(r[q * 4 + 3]) + v.w);
+            }
+          }
+        };
+
+        if constexpr (EPI == kEpiBf16 || EPI == kEpiF32 || EPI == kEpiResid) {
+#pragma unroll 1
+          for (int c = 0; c < BLOCK_N / 32; ++c) {
+            uint32_t r[32];
+            load_acc(c * 32, r);
+            const int n0 = n_blk * BLOCK_N + c * 32;
+            if (valid && n0 < args.N) {
+              if constexpr (EPI == kEpiBf16) {
+                __nv_bfloat16* dst =
+                    reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<size_t>(m) * args.ldo + n0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  st_global_v4(dst + q * 8,
+                               pack_bf16(__uint_as_float(r[q * 8 + 0]), __uint_as_float(r[q * 8 + 1])),
+                               pack_bf16(__uint_as_float(r[q * 8 + 2]), __uint_as_float(r[q * 8 + 3])),
+                               pack_bf16(__uint_as_float(r[q * 8 + 4]), __uint_as_float(r[q * 8 + 5])),
+                               pack_bf16(__uint_as_float(r[q * 8 + 6]), __uint_as_float(r[q * 8 + 7])));
+                }
+              } else if constexpr (EPI == kEpiF32) {
+                float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) +
+                                                        static_cast<size_t>(m) * args.ldo + n0);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                  dst[q] = make_float4(__uint_as_float(r[q * 4]), __uint_as_float(r[q * 4 + 1]),
+                                       __uint_as_float(r[q * 4 + 2]), __uint_as_float(r[q * 4 + 3]));
+              } else {
+                float4* dst =
+                    reinterpret_cast<float4*>(args.resid + static_cast<size_t>(m) * args.ldr + n0);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                  float4 h = dst[q];
+                  h.x += __uint_as_float(r[q * 4]);
+                  h.y += __uint_as_float(r[q * 4 + 1]);
+                  h.z += __uint_as_float(r[q * 4 + 2]);
+                  h.w += __uint_as_float(r[q * 4 + 3]);
+                  dst[q] = h;
+                }
+              }
+            }
+          }
+        } else if constexpr (EPI == kEpiSwiglu) {
+          static_assert(BLOCK_N == 256, "gate/up interleave is 128 columns");
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t g[32], u[32];
+            load_acc(c * 32, g);
+            load_acc(128 + c * 32, u);
+            if (valid) {
+              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) +
+                                   static_cast<size_t>(m) * args.ldo + n_blk * 128 + c * 32;
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
-                st_global_v4(dst + q * 8,
-                             pack_bf16(__uint_as_float(r[q * 8 + 0]), __uint_as_float(r[q * 8 + 1])),
-                             pack_bf16(__uint_as_float(r[q * 8 + 2]), __uint_as_float(r[q * 8 + 3])),
-                             pack_bf16(__uint_as_float(r[q * 8 + 4]), __uint_as_float(r[q * 8 + 5])),
-                             pack_bf16(__uint_as_float(r[q * 8 + 6]), __uint_as_float(r[q * 8 + 7])));
-              }
-            } else if constexpr (EPI == kEpiF32) {
-              float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) +
-                                                      static_cast<size_t>(m) * args.ldo + n0);
+                uint32_t w[4];
 #pragma unroll
-              for (int q = 0; q < 8; ++q)
-                dst[q] = make_float4(__uint_as_float(r[q * 4]), __uint_as_float(r[q * 4 + 1]),
-                                     __uint_as_float(r[q * 4 + 2]), __uint_as_float(r[q * 4 + 3]));
-            } else {
-              float4* dst =
-                  reinterpret_cast<float4*>(args.resid + static_cast<size_t>(m) * args.ldr + n0);
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                float4 h = dst[q];
-                h.x += __uint_as_float(r[q * 4]);
-                h.y += __uint_as_float(r[q * 4 + 1]);
-                h.z += __uint_as_float(r[q * 4 + 2]);
-                h.w += __uint_as_float(r[q * 4 + 3]);
-                dst[q] = h;
+                for (int e = 0; e < 4; ++e) {
+                  const int i = q * 8 + e * 2;
+                  float a0 = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
+                  float a1 = silu_f(__uint_as_float(g[i + 1])) * __uint_as_float(u[i + 1]);
+                  w[e] = pack_bf16(a0, a1);
+                }
+                st_global_v4(dst + q * 8, w[0], w[1], w[2], w[3]);
               }
             }
           }
-        }
-      } else if constexpr (EPI == kEpiSwiglu) {
-        static_assert(BLOCK_N == 256, "gate/up interleave is 128 columns");
+        } else if constexpr (EPI == kEpiQkv) {
+          const int hd = args.head_dim;
+          const int half = hd >> 1;
+          const int heads_per_tile = BLOCK_N / hd;
+          const long long pos = args.pos0 + m;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t g[32], u[32];
-          tmem_ld32(tbase + c * 32, g);
-          tmem_ld32(tbase + 128 + c * 32, u);
-          tmem_ld_wait();
-          if (valid) {
-            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) +
-                                 static_cast<size_t>(m) * args.ldo + n_blk * 128 + c * 32;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint32_t w[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int i = q * 8 + e * 2;
-                float a0 = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
-                float a1 = silu_f(__uint_as_float(g[i + 1])) * __uint_as_float(u[i + 1]);
-                w[e] = pack_bf16(a0, a1);
-              }
-              st_global_v4(dst + q * 8, w[0], w[1], w[2], w[3]);
-            }
-          }
-        }
-      } else if constexpr (EPI == kEpiQkv) {
-        const int hd = args.head_dim;
-        const int half = hd >> 1;
-        const int heads_per_tile = BLOCK_N / hd;
-        const long long pos = args.pos0 + m;
+          for (int h = 0; h < heads_per_tile; ++h) {
+            const int head = n_blk * heads_per_tile + h;
+            const int region =
+                head < args.n_q_heads ? 0 : (head < args.n_q_heads + args.n_kv_heads ? 1 : 2);
 #pragma unroll 1
-        for (int h = 0; h < heads_per_tile; ++h) {
-          const int head = n_blk * heads_per_tile + h;
-          const int region = head < args.n_q_heads ? 0 : (head < args.n_q_heads + args.n_kv_heads ? 1 : 2);
-#pragma unroll 1
-          for (int j = 0; j < half / 32; ++j) {
-            uint32_t x0[32], x1[32];
-            tmem_ld32(tbase + h * hd + j * 32, x0);
-            tmem_ld32(tbase + h * hd + half + j * 32, x1);
-            tmem_ld_wait();
-            if (!valid) continue;
-            float o0[32], o1[32];
-            if (region < 2) {
-              const float2* cs = args.rope + pos * half + j * 32;
+            for (int j = 0; j < half / 32; ++j) {
+              uint32_t x0[32], x1[32];
+              load_acc(h * hd + j * 32, x0);
+              load_acc(h * hd + half + j * 32, x1);
+              if (!valid) continue;
+              float o0[32], o1[32];
+              if (region < 2) {
+                const float2* cs = args.rope + pos * half + j * 32;
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const float2 t = cs[i];
-                const float a = __uint_as_float(x0[i]);
-                const float b = __uint_as_float(x1[i]);
-                o0[i] = a * t.x - b * t.y;
-                o1[i] = b * t.x + a * t.y;
+                for (int i = 0; i < 32; ++i) {
+                  const float2 t = cs[i];
+                  const float a = __uint_as_float(x0[i]);
+                  const float b = __uint_as_float(x1[i]);
+                  o0[i] = a * t.x - b * t.y;
+                  o1[i] = b * t.x + a * t.y;
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  o0[i] = __uint_as_float(x0[i]);
+                  o1[i] = __uint_as_float(x1[i]);
+                }
               }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                o0[i] = __uint_as_float(x0[i]);
-                o1[i] = __uint_as_float(x1[i]);
+              __nv_bfloat16* dst;
+              if (region == 0) {
+                dst = args.q_out + static_cast<size_t>(m) * (args.n_q_heads * hd) + head * hd;
+              } else {
+                const int kvh = region == 1 ? head - args.n_q_heads : head - args.n_q_heads - args.n_kv_heads;
+                const long long lpage = pos / args.page_tokens;
+                const int slot = static_cast<int>(pos - lpage * args.page_tokens);
+                const long long phys = args.block_table[lpage];
+                const size_t off =
+                    ((((static_cast<size_t>(phys) * args.n_layers + args.layer) * 2 + (region - 1)) *
+                          args.n_kv_heads + kvh) * args.page_tokens + slot) * static_cast<size_t>(hd);
+                dst = args.kv_pool + off;
               }
-            }
-            __nv_bfloat16* dst;
-            if (region == 0) {
-              dst = args.q_out + static_cast<size_t>(m) * (args.n_q_heads * hd) + head * hd;
-            } else {
-              const int kvh = region == 1 ? head - args.n_q_heads : head - args.n_q_heads - args.n_kv_heads;
-              const long long lpage = pos / args.page_tokens;
-              const int slot = static_cast<int>(pos - lpage * args.page_tokens);
-              const long long phys = args.block_table[lpage];
-              const size_t off =
-                  ((((static_cast<size_t>(phys) * args.n_layers + args.layer) * 2 + (region - 1)) *
-                        args.n_kv_heads + kvh) * args.page_tokens + slot) * static_cast<size_t>(hd);
-              dst = args.kv_pool + off;
-            }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              st_global_v4(dst + j * 32 + q * 8, pack_bf16(o0[q * 8 + 0], o0[q * 8 + 1]),
-                           pack_bf16(o0[q * 8 + 2], o0[q * 8 + 3]), pack_bf16(o0[q * 8 + 4], o0[q * 8 + 5]),
-                           pack_bf16(o0[q * 8 + 6], o0[q * 8 + 7]));
-              st_global_v4(dst + half + j * 32 + q * 8, pack_bf16(o1[q * 8 + 0], o1[q * 8 + 1]),
-                           pack_bf16(o1[q * 8 + 2], o1[q * 8 + 3]), pack_bf16(o1[q * 8 + 4], o1[q * 8 + 5]),
-                           pack_bf16(o1[q * 8 + 6], o1[q * 8 + 7]));
+              for (int q = 0; q < 4; ++q) {
+                st_global_v4(dst + j * 32 + q * 8, pack_bf16(o0[q * 8 + 0], o0[q * 8 + 1]),
+                             pack_bf16(o0[q * 8 + 2], o0[q * 8 + 3]), pack_bf16(o0[q * 8 + 4], o0[q * 8 + 5]),
+                             pack_bf16(o0[q * 8 + 6], o0[q * 8 + 7]));
+                st_global_v4(dst + half + j * 32 + q * 8, pack_bf16(o1[q * 8 + 0], o1[q * 8 + 1]),
+                             pack_bf16(o1[q * 8 + 2], o1[q * 8 + 3]), pack_bf16(o1[q * 8 + 4], o1[q * 8 + 5]),
+                             pack_bf16(o1[q * 8 + 6], o1[q * 8 + 7]));
+              }
             }
           }
         }
