@@ -189,6 +189,11 @@ CAKE_API int cake_model_kernel_stats(cake_model* m, cake_kernel_stat* out /* [CA
 CAKE_API int cake_model_launch_count(cake_model* m, long long* n, int reset);
 
 /* ---------------------------------------------------------- unit entry points */
+/* Projection GEMM schedule for subsequent launches (bit flags): bit0 stream-K
+ * instead of whole tiles (+ exact split-K), bit1 disable the 2-SM
+ * (cta_group::2) kernel for M > 128, bit2 weight-multicast clusters in the
+ * 1-SM kernel. Default 0. */
+CAKE_API int cake_gemm_set_schedule(int schedule);
 /* C = A · B^T for bf16 row-major A [M, K], B [N, K]; epi 0: bf16 C, 1: fp32 C,
  * 2: fp32 C += . block_n 128 or 256. For tests and microbenchmarks. */
 CAKE_API int cake_gemm(const void* dA, const void* dB, void* dC, int M, int N, int K, int epi, int block_n,

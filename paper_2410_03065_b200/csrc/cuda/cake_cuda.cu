@@ -20,6 +20,7 @@
 #include "cake_cuda.h"
 #include "elementwise.cuh"
 #include "gemm.cuh"
+#include "gemm2.cuh"
 #include "skinny.cuh"
 
 using namespace cake_dev;
@@ -129,6 +130,8 @@ struct StreamKScratch {
   std::mutex mu;
 };
 StreamKScratch g_sk;
+int g_gemm_schedule = 0;  // 0 whole tiles (+ exact split-K when tiles < SM pairs), 1 stream-K
+int g_gemm_2sm = 1;       // 1: M > 128 projections use the 2-SM (cta_group::2) kernel
 
 int streamk_scratch(float** ws, int** flags, int* epoch) {
   std::lock_guard<std::mutex> lk(g_sk.mu);
@@ -144,11 +147,21 @@ int streamk_scratch(float** ws, int** flags, int* epoch) {
   return CAKE_OK;
 }
 
+// Cluster size for a chunk of M rows: its m-blocks share every weight k-block.
+int g_gemm_cluster = 0;  // 1-SM kernel: multicast weight k-blocks across the chunk's m-blocks
+int cluster_size_for(int M) {
+  const int mb = (M + kGemmBlockM - 1) / kGemmBlockM;
+  if (!g_gemm_cluster) return 1;
+  return mb <= 1 ? 1 : (mb == 2 ? 2 : 4);
+}
+int cs_index(int cs) { return cs == 1 ? 0 : (cs == 2 ? 1 : 2); }
+
 template <int BN, int EPI>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaStream_t s) {
   using Cfg = GemmCfg<BN>;
   auto kern = gemm_tc_kernel<BN, EPI>;
   static bool configured = false;
+  static int max_clusters[3] = {0, 0, 0};
   if (!configured) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
     configured = true;
@@ -156,17 +169,110 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaSt
   a.num_m_blocks = (a.M + kGemmBlockM - 1) / kGemmBlockM;
   a.num_n_blocks = a.N / BN;
   a.num_k_blocks = a.K / kGemmBlockK;
-  const long long units = static_cast<long long>(a.num_m_blocks) * a.num_n_blocks * a.num_k_blocks;
-  // every CTA gets >= 8 k-blocks (and >= 1 unit, so no CTA is empty)
-  const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(num_sms(), units / 8)));
+  a.cs = cluster_size_for(a.M);
+  const int ci = cs_index(a.cs);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = a.cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (max_clusters[ci] == 0) {
+    cfg.gridDim = dim3(a.cs * 16);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = num_sms() / a.cs;
+    }
+    max_clusters[ci] = std::min(n, num_sms() / a.cs);
+  }
+  const int m_groups = (a.num_m_blocks + a.cs - 1) / a.cs;
+  const long long units = static_cast<long long>(m_groups) * a.num_n_blocks * a.num_k_blocks;
+  a.whole_tiles = g_gemm_schedule == 0;
+  // stream-K: every cluster gets >= 8 k-blocks (>= 1 unit, so none is empty); all clusters co-resident
+  const long long work = a.whole_tiles ? static_cast<long long>(m_groups) * a.num_n_blocks : units / 8;
+  const int clusters = static_cast<int>(std::max<long long>(1, std::min<long long>(max_clusters[ci], work)));
+  cfg.gridDim = dim3(clusters * a.cs);
   CKS(streamk_scratch(&a.sk_ws, &a.sk_flags, &a.epoch));
-  kern<<<grid, kGemmThreads, Cfg::kSmemBytes, s>>>(ta, tb, a);
-  CKL();
+  CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, a));
   return CAKE_OK;
 }
 
-int gemm_dispatch(int bn, int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a,
+// 2-SM GEMM: pairs of CTAs on 256 x 256 tiles. Few tiles (O / down at M = 512:
+// 32) are split along K into S equal parts so the pairs fill the GPU; the
+// k = 0 part owns the tile and adds the others (deterministic order).
+template <int EPI>
+int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, cudaStream_t s) {
+  using Cfg = Gemm2Cfg;
+  auto kern = gemm2_tc_kernel<EPI>;
+  static bool configured = false;
+  static int max_pairs = 0;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (!configured) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+    cfg.gridDim = dim3(32);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = num_sms() / 2;
+    }
+    max_pairs = std::min(n, num_sms() / 2);
+    configured = true;
+  }
+  a.num_m_blocks = (a.M + kGemmBlockM - 1) / kGemmBlockM;
+  a.num_n_blocks = a.N / kGemm2BlockN;
+  a.num_k_blocks = a.K / kGemmBlockK;
+  a.cs = 2;
+  const int m_pairs = (a.num_m_blocks + 1) / 2;
+  const int tiles = m_pairs * a.num_n_blocks;
+  int pairs;
+  if (g_gemm_schedule == 1) {
+    a.whole_tiles = 0;
+    const long long units = static_cast<long long>(tiles) * a.num_k_blocks;
+    pairs = static_cast<int>(std::max<long long>(1, std::min<long long>(max_pairs, units / 8)));
+  } else {
+    int split = 1;
+    while (tiles * (split + 1) <= max_pairs && a.num_k_blocks % (split + 1) == 0 &&
+           a.num_k_blocks / (split + 1) >= 8)
+      ++split;
+    a.whole_tiles = split == 1 ? 1 : 0;
+    pairs = split == 1 ? std::min(tiles, max_pairs) : tiles * split;
+  }
+  cfg.gridDim = dim3(2 * pairs);
+  CKS(streamk_scratch(&a.sk_ws, &a.sk_flags, &a.epoch));
+  CK(cudaLaunchKernelEx(&cfg, kern, ta, tb_half, a));
+  return CAKE_OK;
+}
+
+int gemm_dispatch(int bn, int epi, const CUtensorMap& ta, const CUtensorMap* tb3, const GemmArgs& a,
                   cudaStream_t s) {
+  if (g_gemm_2sm && a.M > kGemmBlockM && a.N % kGemm2BlockN == 0 && (bn == 256 || epi != kEpiQkv)) {
+    // B maps: index k holds box rows bn >> k; the 2-SM kernel loads 128-row halves
+    const CUtensorMap& half = tb3[bn == 256 ? 1 : 0];
+    switch (epi) {
+      case kEpiBf16: return launch_gemm2<kEpiBf16>(ta, half, a, s);
+      case kEpiF32: return launch_gemm2<kEpiF32>(ta, half, a, s);
+      case kEpiResid: return launch_gemm2<kEpiResid>(ta, half, a, s);
+      case kEpiSwiglu: return launch_gemm2<kEpiSwiglu>(ta, half, a, s);
+      case kEpiQkv: return launch_gemm2<kEpiQkv>(ta, half, a, s);
+    }
+  }
+  const CUtensorMap& tb = tb3[cs_index(cluster_size_for(a.M))];
   if (bn == 256) {
     switch (epi) {
       case kEpiBf16: return launch_gemm<256, kEpiBf16>(ta, tb, a, s);
@@ -202,7 +308,7 @@ struct LayerWeights {
   bf16* wd = nullptr;    // [H, F]                   local input columns
   bf16* ln1 = nullptr;
   bf16* ln2 = nullptr;
-  CUtensorMap m_qkv, m_o, m_gu, m_d;
+  CUtensorMap m_qkv[3], m_o[3], m_gu[3], m_d[3];  // B box = BLOCK_N / cluster size (1, 2, 4)
 };
 
 struct ProfPair {
@@ -545,7 +651,7 @@ int rmsnorm(cake_model* m, const bf16* gamma, long long row0, int rows, const in
 }
 
 // Row-parallel projection output: residual += acc (TP: via all-reduce of partials).
-int row_parallel(cake_model* m, int kind, const CUtensorMap& ta, const CUtensorMap& tb, int K, int M,
+int row_parallel(cake_model* m, int kind, const CUtensorMap& ta, const CUtensorMap* tb, int K, int M,
                  const int32_t* abort_flag, cudaStream_t s) {
   GemmArgs g{};
   g.M = M;
@@ -812,10 +918,13 @@ int cake_model_create(const cake_model_config* cfg, cake_model** out) {
     if ((st = init_tensor(lw.wd, H, F, 0, r * F, c.ffn, 0, 0, seed, tid_layer(l, kWdown), s_f, s))) return bail(st);
     if ((st = fill(lw.ln1, H, 1.0f, s))) return bail(st);
     if ((st = fill(lw.ln2, H, 1.0f, s))) return bail(st);
-    if ((st = make_map(&lw.m_qkv, lw.wqkv, m->qkv_rows, H, m->bn_qkv))) return bail(st);
-    if ((st = make_map(&lw.m_o, lw.wo, H, m->nq * hd, 128))) return bail(st);
-    if ((st = make_map(&lw.m_gu, lw.wgu, 2 * F, H, 256))) return bail(st);
-    if ((st = make_map(&lw.m_d, lw.wd, H, F, 128))) return bail(st);
+    for (int ci = 0; ci < 3; ++ci) {
+      const uint32_t div = 1u << ci;  // cluster size 1, 2, 4
+      if ((st = make_map(&lw.m_qkv[ci], lw.wqkv, m->qkv_rows, H, m->bn_qkv / div))) return bail(st);
+      if ((st = make_map(&lw.m_o[ci], lw.wo, H, m->nq * hd, 128 / div))) return bail(st);
+      if ((st = make_map(&lw.m_gu[ci], lw.wgu, 2 * F, H, 256 / div))) return bail(st);
+      if ((st = make_map(&lw.m_d[ci], lw.wd, H, F, 128 / div))) return bail(st);
+    }
   }
   m->embed = take(V * H);
   m->lm_head = take(V * H);
@@ -1077,12 +1186,22 @@ int cake_kv_gather(cake_model* m, void* d_staging, long long chunk_start, int ch
                     false, S(stream));
 }
 
+int cake_gemm_set_schedule(int schedule) {
+  // bit 0: stream-K; bit 1: disable the 2-SM kernel; bit 2: 1-SM weight multicast clusters
+  if (schedule < 0 || schedule > 7) return fail(CAKE_EINVAL, "schedule bits: 1 stream-K, 2 no-2SM, 4 multicast");
+  g_gemm_schedule = schedule & 1;
+  g_gemm_2sm = (schedule & 2) ? 0 : 1;
+  g_gemm_cluster = (schedule & 4) ? 1 : 0;
+  return CAKE_OK;
+}
+
 int cake_gemm(const void* dA, const void* dB, void* dC, int M, int N, int K, int epi, int block_n, void* stream) {
   if (M < 1 || N < 1 || K < 64 || K % 64 || N % block_n) return fail(CAKE_EINVAL, "gemm: bad shape");
   if (epi < 0 || epi > 2) return fail(CAKE_EINVAL, "gemm: epi must be 0..2");
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb[3];
   CKS(make_map(&ta, dA, static_cast<uint64_t>(M), static_cast<uint64_t>(K), 128));
-  CKS(make_map(&tb, dB, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint32_t>(block_n)));
+  for (int ci = 0; ci < 3; ++ci)
+    CKS(make_map(&tb[ci], dB, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint32_t>(block_n >> ci)));
   GemmArgs g{};
   g.M = M;
   g.N = N;

@@ -15,6 +15,14 @@
 // segment (processed last by it) waits for those flags and adds the partials
 // in k order before the fused epilogue.
 //
+// Clusters: the cs (<= 4) m-blocks of a chunk (M <= 512) form one thread-
+// block cluster that walks the (n-block, k-block) units in lockstep. Each CTA
+// TMA-loads 1/cs of the weight k-block and multicasts it to the whole
+// cluster, and each CTA's MMA completion is multicast to every CTA's
+// empty barrier, so a weight byte leaves HBM once and crosses L2->SM once
+// per cluster (not once per m-block). Stream-K then splits the unit list
+// across clusters (partials/owners per CTA as below).
+//
 // Roles (192 threads):
 //   warp 0      TMA producer: A/B k-blocks into a kStages smem ring (SW128)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
@@ -56,6 +64,8 @@ struct GemmArgs {
   float* sk_ws;             // [gridDim.x][128][BLOCK_N] partial tiles
   int* sk_flags;            // [gridDim.x] = epoch when the CTA's partial is published
   int epoch;
+  int whole_tiles;          // 1: classic persistent schedule (tile t -> CTA t % grid), no splits
+  int cs;                   // cluster size = CTAs sharing (multicasting) each weight k-block, one m-block each
 };
 
 constexpr int kGemmBlockM = 128;
@@ -78,13 +88,28 @@ __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)
 struct StreamK {
   long long total, u, u_end;
   int nk, grid;
-  __device__ StreamK(long long units, int num_k, int cta, int g) : total(units), nk(num_k), grid(g) {
+  int tile_mode = 0, next_tile = 0, n_tiles = 0;
+  __device__ StreamK(long long units, int num_k, int cta, int g, int whole_tiles = 0)
+      : total(units), nk(num_k), grid(g) {
     u = units * cta / g;
     u_end = units * (cta + 1) / g;
+    if (whole_tiles) {
+      tile_mode = 1;
+      next_tile = cta;
+      n_tiles = static_cast<int>(units / num_k);
+    }
   }
   // CTA that owns unit v under the balanced split
   __device__ int cta_of(long long v) const { return static_cast<int>(((v + 1) * grid + total - 1) / total - 1); }
   __device__ bool next(int& tile, int& kb0, int& kb1) {
+    if (tile_mode) {
+      if (next_tile >= n_tiles) return false;
+      tile = next_tile;
+      next_tile += grid;
+      kb0 = 0;
+      kb1 = nk;
+      return true;
+    }
     if (u >= u_end) return false;
     tile = static_cast<int>(u / nk);
     kb0 = static_cast<int>(u - static_cast<long long>(tile) * nk);
@@ -94,6 +119,185 @@ struct StreamK {
     return true;
   }
 };
+
+// Fused epilogue of one accumulator tile: this thread owns TMEM lane `row`
+// (output row m). partial: publish the fp32 tile into workspace slot my_slot
+// and raise its flag; otherwise wait for n_parts partial slots (first_slot +
+// p * slot_stride, k order), add them, and apply the fused op.
+template <int BLOCK_N, int EPI>
+__device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t tbase, int row, int m, int n_blk,
+                                              bool partial, int my_slot, int first_slot, int n_parts,
+                                              int slot_stride, int ep_tid) {
+  const bool valid = m < args.M;
+  if (partial) {
+    // ---- partial segment: publish the fp32 tile in this CTA's slot
+    float4* slot = reinterpret_cast<float4*>(args.sk_ws + (static_cast<size_t>(my_slot) * kGemmBlockM + row) * BLOCK_N);
+#pragma unroll 1
+    for (int c = 0; c < BLOCK_N / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(tbase + c * 32, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        slot[c * 8 + q] = make_float4(__uint_as_float(r[q * 4]), __uint_as_float(r[q * 4 + 1]),
+                                      __uint_as_float(r[q * 4 + 2]), __uint_as_float(r[q * 4 + 3]));
+    }
+    __threadfence();
+    named_bar_sync(1, 128);
+    if (ep_tid == 0) atomicExch(args.sk_flags + my_slot, args.epoch);
+  } else {
+    // ---- full tile, or the k = 0 owner of a split tile: wait for the other parts
+    if (n_parts > 0) {
+      if (ep_tid == 0) {
+        for (int p = 0; p < n_parts; ++p)
+          while (*(volatile int*)(args.sk_flags + first_slot + p * slot_stride) != args.epoch) __nanosleep(64);
+        __threadfence();
+      }
+      named_bar_sync(1, 128);
+    }
+    // accumulator chunk c (32 columns) of this thread's row, partials added in k order
+    auto load_acc = [&](int col, uint32_t (&r)[32]) {
+      tmem_ld32(tbase + col, r);
+      tmem_ld_wait();
+      for (int p = 0; p < n_parts; ++p) {
+        const float4* part = reinterpret_cast<const float4*>(
+            args.sk_ws + (static_cast<size_t>(first_slot + p * slot_stride) * kGemmBlockM + row) * BLOCK_N + col);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 v = __ldcg(part + q);
+          r[q * 4] = __float_as_uint(__uint_as_float(r[q * 4]) + v.x);
+          r[q * 4 + 1] = __float_as_uint(__uint_as_float(r[q * 4 + 1]) + v.y);
+          r[q * 4 + 2] = __float_as_uint(__uint_as_float(r[q * 4 + 2]) + v.z);
+          r[q * 4 + 3] = __float_as_uint(__uint_as_float(r[q * 4 + 3]) + v.w);
+        }
+      }
+    };
+
+    if constexpr (EPI == kEpiBf16 || EPI == kEpiF32 || EPI == kEpiResid) {
+#pragma unroll 1
+      for (int c = 0; c < BLOCK_N / 32; ++c) {
+        uint32_t r[32];
+        load_acc(c * 32, r);
+        const int n0 = n_blk * BLOCK_N + c * 32;
+        if (valid && n0 < args.N) {
+          if constexpr (EPI == kEpiBf16) {
+            __nv_bfloat16* dst =
+                reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<size_t>(m) * args.ldo + n0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              st_global_v4(dst + q * 8,
+                           pack_bf16(__uint_as_float(r[q * 8 + 0]), __uint_as_float(r[q * 8 + 1])),
+                           pack_bf16(__uint_as_float(r[q * 8 + 2]), __uint_as_float(r[q * 8 + 3])),
+                           pack_bf16(__uint_as_float(r[q * 8 + 4]), __uint_as_float(r[q * 8 + 5])),
+                           pack_bf16(__uint_as_float(r[q * 8 + 6]), __uint_as_float(r[q * 8 + 7])));
+            }
+          } else if constexpr (EPI == kEpiF32) {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) +
+                                                    static_cast<size_t>(m) * args.ldo + n0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              dst[q] = make_float4(__uint_as_float(r[q * 4]), __uint_as_float(r[q * 4 + 1]),
+                                   __uint_as_float(r[q * 4 + 2]), __uint_as_float(r[q * 4 + 3]));
+          } else {
+            float4* dst =
+                reinterpret_cast<float4*>(args.resid + static_cast<size_t>(m) * args.ldr + n0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 h = dst[q];
+              h.x += __uint_as_float(r[q * 4]);
+              h.y += __uint_as_float(r[q * 4 + 1]);
+              h.z += __uint_as_float(r[q * 4 + 2]);
+              h.w += __uint_as_float(r[q * 4 + 3]);
+              dst[q] = h;
+            }
+          }
+        }
+      }
+    } else if constexpr (EPI == kEpiSwiglu) {
+      static_assert(BLOCK_N == 256, "gate/up interleave is 128 columns");
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t g[32], u[32];
+        load_acc(c * 32, g);
+        load_acc(128 + c * 32, u);
+        if (valid) {
+          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) +
+                               static_cast<size_t>(m) * args.ldo + n_blk * 128 + c * 32;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i = q * 8 + e * 2;
+              float a0 = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
+              float a1 = silu_f(__uint_as_float(g[i + 1])) * __uint_as_float(u[i + 1]);
+              w[e] = pack_bf16(a0, a1);
+            }
+            st_global_v4(dst + q * 8, w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+    } else if constexpr (EPI == kEpiQkv) {
+      const int hd = args.head_dim;
+      const int half = hd >> 1;
+      const int heads_per_tile = BLOCK_N / hd;
+      const long long pos = args.pos0 + m;
+#pragma unroll 1
+      for (int h = 0; h < heads_per_tile; ++h) {
+        const int head = n_blk * heads_per_tile + h;
+        const int region =
+            head < args.n_q_heads ? 0 : (head < args.n_q_heads + args.n_kv_heads ? 1 : 2);
+#pragma unroll 1
+        for (int j = 0; j < half / 32; ++j) {
+          uint32_t x0[32], x1[32];
+          load_acc(h * hd + j * 32, x0);
+          load_acc(h * hd + half + j * 32, x1);
+          if (!valid) continue;
+          float o0[32], o1[32];
+          if (region < 2) {
+            const float2* cs = args.rope + pos * half + j * 32;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float2 t = cs[i];
+              const float a = __uint_as_float(x0[i]);
+              const float b = __uint_as_float(x1[i]);
+              o0[i] = a * t.x - b * t.y;
+              o1[i] = b * t.x + a * t.y;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              o0[i] = __uint_as_float(x0[i]);
+              o1[i] = __uint_as_float(x1[i]);
+            }
+          }
+          __nv_bfloat16* dst;
+          if (region == 0) {
+            dst = args.q_out + static_cast<size_t>(m) * (args.n_q_heads * hd) + head * hd;
+          } else {
+            const int kvh = region == 1 ? head - args.n_q_heads : head - args.n_q_heads - args.n_kv_heads;
+            const long long lpage = pos / args.page_tokens;
+            const int slot = static_cast<int>(pos - lpage * args.page_tokens);
+            const long long phys = args.block_table[lpage];
+            const size_t off =
+                ((((static_cast<size_t>(phys) * args.n_layers + args.layer) * 2 + (region - 1)) *
+                      args.n_kv_heads + kvh) * args.page_tokens + slot) * static_cast<size_t>(hd);
+            dst = args.kv_pool + off;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            st_global_v4(dst + j * 32 + q * 8, pack_bf16(o0[q * 8 + 0], o0[q * 8 + 1]),
+                         pack_bf16(o0[q * 8 + 2], o0[q * 8 + 3]), pack_bf16(o0[q * 8 + 4], o0[q * 8 + 5]),
+                         pack_bf16(o0[q * 8 + 6], o0[q * 8 + 7]));
+            st_global_v4(dst + half + j * 32 + q * 8, pack_bf16(o1[q * 8 + 0], o1[q * 8 + 1]),
+                         pack_bf16(o1[q * 8 + 2], o1[q * 8 + 3]), pack_bf16(o1[q * 8 + 4], o1[q * 8 + 5]),
+                         pack_bf16(o1[q * 8 + 6], o1[q * 8 + 7]));
+          }
+        }
+      }
+    }
+  }
+}
 
 template <int BLOCK_N, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -127,7 +331,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_prefetch_desc(&tmap_b);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], args.cs);  // every CTA of the cluster must release the stage
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
@@ -142,26 +346,39 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int nk = args.num_k_blocks;
-  const long long units = static_cast<long long>(args.num_m_blocks) * args.num_n_blocks * nk;
+  const int cs = args.cs;
+  const int rank = cs > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int cluster = blockIdx.x / cs;
+  const int n_clusters = gridDim.x / cs;
+  const uint16_t mc_mask = static_cast<uint16_t>((1u << cs) - 1u);
+  // unit space: (tile, k) with tile = n-block x (m-group of cs m-blocks); this CTA takes m-block rank
+  const int m_groups = (args.num_m_blocks + cs - 1) / cs;
+  const long long units = static_cast<long long>(m_groups) * args.num_n_blocks * nk;
   int tile, kb0, kb1;
+  if (cs > 1) cluster_sync();  // peers' barriers are initialised before any multicast
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       const uint64_t pol_w = policy_evict_last();   // weights: reused by the other m-blocks
-      StreamK sk(units, nk, blockIdx.x, gridDim.x);
+      StreamK sk(units, nk, cluster, n_clusters, args.whole_tiles);
       int stage = 0;
       uint32_t phase = 0;
+      const int b_rows = BLOCK_N / cs;  // this CTA's share of the weight k-block
       while (sk.next(tile, kb0, kb1)) {
-        const int m_blk = tile % args.num_m_blocks;
-        const int n_blk = tile / args.num_m_blocks;
+        const int m_blk = (tile % m_groups) * cs + rank;
+        const int n_blk = tile / m_groups;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
           tma_load_2d(smem_a + stage * Cfg::kABytes, &tmap_a, &full_bar[stage], kb * kGemmBlockK,
                       m_blk * kGemmBlockM);
-          tma_load_2d_hint(smem_b + stage * Cfg::kBBytes, &tmap_b, &full_bar[stage],
-                           kb * kGemmBlockK, n_blk * BLOCK_N, pol_w);
+          if (cs > 1)
+            tma_load_2d_mc(smem_b + stage * Cfg::kBBytes + rank * b_rows * 128, &tmap_b, &full_bar[stage],
+                           kb * kGemmBlockK, n_blk * BLOCK_N + rank * b_rows, mc_mask, pol_w);
+          else
+            tma_load_2d_hint(smem_b + stage * Cfg::kBBytes, &tmap_b, &full_bar[stage], kb * kGemmBlockK,
+                             n_blk * BLOCK_N, pol_w);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1u;
@@ -173,7 +390,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       // ------------------------------------------------ MMA issuer
       constexpr uint32_t idesc = umma_idesc_bf16(kGemmBlockM, BLOCK_N);
-      StreamK sk(units, nk, blockIdx.x, gridDim.x);
+      StreamK sk(units, nk, cluster, n_clusters, args.whole_tiles);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -192,7 +409,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             umma_bf16_ss(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32),
                          idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty_bar[stage]);
+          if (cs > 1)
+            umma_commit_mc(&empty_bar[stage], mc_mask);
+          else
+            umma_commit(&empty_bar[stage]);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1u;
@@ -210,189 +430,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int ew = warp & 3;  // TMEM lane quarter this warp may access
     const int row = ew * 32 + static_cast<int>(lane);
     const int ep_tid = threadIdx.x - 64;  // 0..127
-    StreamK sk(units, nk, blockIdx.x, gridDim.x);
+    StreamK sk(units, nk, cluster, n_clusters, args.whole_tiles);
     int acc = 0;
     uint32_t acc_phase = 0;
     while (sk.next(tile, kb0, kb1)) {
-      const int m_blk = tile % args.num_m_blocks;
-      const int n_blk = tile / args.num_m_blocks;
+      const int m_blk = (tile % m_groups) * cs + rank;
+      const int n_blk = tile / m_groups;
       const int m = m_blk * kGemmBlockM + row;
-      const bool valid = m < args.M;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase =
           tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * BLOCK_N);
 
-      if (kb0 > 0) {
-        // ---- partial segment: publish the fp32 tile in this CTA's slot
-        float4* slot = reinterpret_cast<float4*>(args.sk_ws + (static_cast<size_t>(blockIdx.x) * kGemmBlockM + row) * BLOCK_N);
-#pragma unroll 1
-        for (int c = 0; c < BLOCK_N / 32; ++c) {
-          uint32_t r[32];
-          tmem_ld32(tbase + c * 32, r);
-          tmem_ld_wait();
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            slot[c * 8 + q] = make_float4(__uint_as_float(r[q * 4]), __uint_as_float(r[q * 4 + 1]),
-                                          __uint_as_float(r[q * 4 + 2]), __uint_as_float(r[q * 4 + 3]));
+      {
+        const bool partial = kb0 > 0;
+        int first_part = 0, n_parts = 0;
+        if (!partial && kb1 < nk) {
+          const long long u_tile = static_cast<long long>(tile) * nk;
+          first_part = sk.cta_of(u_tile) + 1;
+          n_parts = sk.cta_of(u_tile + nk - 1) - first_part + 1;
         }
-        __threadfence();
-        named_bar_sync(1, 128);
-        if (ep_tid == 0) atomicExch(args.sk_flags + blockIdx.x, args.epoch);
-      } else {
-        // ---- full tile, or the k = 0 owner of a split tile: wait for the other parts
-        const long long u_tile = static_cast<long long>(tile) * nk;
-        const int first_part = sk.cta_of(u_tile) + 1;
-        const int last_part = kb1 < nk ? sk.cta_of(u_tile + nk - 1) : first_part - 1;
-        if (last_part >= first_part) {
-          if (ep_tid == 0) {
-            for (int p = first_part; p <= last_part; ++p)
-              while (*(volatile int*)(args.sk_flags + p) != args.epoch) __nanosleep(64);
-            __threadfence();
-          }
-          named_bar_sync(1, 128);
-        }
-        // accumulator chunk c (32 columns) of this thread's row, partials added in k order
-        auto load_acc = [&](int col, uint32_t (&r)[32]) {
-          tmem_ld32(tbase + col, r);
-          tmem_ld_wait();
-          for (int p = first_part; p <= last_part; ++p) {
-            const float4* part =
-                reinterpret_cast<const float4*>(args.sk_ws + (static_cast<size_t>(p) * kGemmBlockM + row) * BLOCK_N + col);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 v = __ldcg(part + q);
-              r[q * 4] = __float_as_uint(__uint_as_float(r[q * 4]) + v.x);
-              r[q * 4 + 1] = __float_as_uint(__uint_as_float(r[q * 4 + 1]) + v.y);
-              r[q * 4 + 2] = __float_as_uint(__uint_as_float(r[q * 4 + 2]) + v.z);
-              r[q * 4 + 3] = __float_as_uint(__uint_as_float(r[q * 4 + 3]) + v.w);
-            }
-          }
-        };
-
-        if constexpr (EPI == kEpiBf16 || EPI == kEpiF32 || EPI == kEpiResid) {
-#pragma unroll 1
-          for (int c = 0; c < BLOCK_N / 32; ++c) {
-            uint32_t r[32];
-            load_acc(c * 32, r);
-            const int n0 = n_blk * BLOCK_N + c * 32;
-            if (valid && n0 < args.N) {
-              if constexpr (EPI == kEpiBf16) {
-                __nv_bfloat16* dst =
-                    reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<size_t>(m) * args.ldo + n0;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  st_global_v4(dst + q * 8,
-                               pack_bf16(__uint_as_float(r[q * 8 + 0]), __uint_as_float(r[q * 8 + 1])),
-                               pack_bf16(__uint_as_float(r[q * 8 + 2]), __uint_as_float(r[q * 8 + 3])),
-                               pack_bf16(__uint_as_float(r[q * 8 + 4]), __uint_as_float(r[q * 8 + 5])),
-                               pack_bf16(__uint_as_float(r[q * 8 + 6]), __uint_as_float(r[q * 8 + 7])));
-                }
-              } else if constexpr (EPI == kEpiF32) {
-                float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) +
-                                                        static_cast<size_t>(m) * args.ldo + n0);
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                  dst[q] = make_float4(__uint_as_float(r[q * 4]), __uint_as_float(r[q * 4 + 1]),
-                                       __uint_as_float(r[q * 4 + 2]), __uint_as_float(r[q * 4 + 3]));
-              } else {
-                float4* dst =
-                    reinterpret_cast<float4*>(args.resid + static_cast<size_t>(m) * args.ldr + n0);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                  float4 h = dst[q];
-                  h.x += __uint_as_float(r[q * 4]);
-                  h.y += __uint_as_float(r[q * 4 + 1]);
-                  h.z += __uint_as_float(r[q * 4 + 2]);
-                  h.w += __uint_as_float(r[q * 4 + 3]);
-                  dst[q] = h;
-                }
-              }
-            }
-          }
-        } else if constexpr (EPI == kEpiSwiglu) {
-          static_assert(BLOCK_N == 256, "gate/up interleave is 128 columns");
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            uint32_t g[32], u[32];
-            load_acc(c * 32, g);
-            load_acc(128 + c * 32, u);
-            if (valid) {
-              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) +
-                                   static_cast<size_t>(m) * args.ldo + n_blk * 128 + c * 32;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                uint32_t w[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const int i = q * 8 + e * 2;
-                  float a0 = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
-                  float a1 = silu_f(__uint_as_float(g[i + 1])) * __uint_as_float(u[i + 1]);
-                  w[e] = pack_bf16(a0, a1);
-                }
-                st_global_v4(dst + q * 8, w[0], w[1], w[2], w[3]);
-              }
-            }
-          }
-        } else if constexpr (EPI == kEpiQkv) {
-          const int hd = args.head_dim;
-          const int half = hd >> 1;
-          const int heads_per_tile = BLOCK_N / hd;
-          const long long pos = args.pos0 + m;
-#pragma unroll 1
-          for (int h = 0; h < heads_per_tile; ++h) {
-            const int head = n_blk * heads_per_tile + h;
-            const int region =
-                head < args.n_q_heads ? 0 : (head < args.n_q_heads + args.n_kv_heads ? 1 : 2);
-#pragma unroll 1
-            for (int j = 0; j < half / 32; ++j) {
-              uint32_t x0[32], x1[32];
-              load_acc(h * hd + j * 32, x0);
-              load_acc(h * hd + half + j * 32, x1);
-              if (!valid) continue;
-              float o0[32], o1[32];
-              if (region < 2) {
-                const float2* cs = args.rope + pos * half + j * 32;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  const float2 t = cs[i];
-                  const float a = __uint_as_float(x0[i]);
-                  const float b = __uint_as_float(x1[i]);
-                  o0[i] = a * t.x - b * t.y;
-                  o1[i] = b * t.x + a * t.y;
-                }
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  o0[i] = __uint_as_float(x0[i]);
-                  o1[i] = __uint_as_float(x1[i]);
-                }
-              }
-              __nv_bfloat16* dst;
-              if (region == 0) {
-                dst = args.q_out + static_cast<size_t>(m) * (args.n_q_heads * hd) + head * hd;
-              } else {
-                const int kvh = region == 1 ? head - args.n_q_heads : head - args.n_q_heads - args.n_kv_heads;
-                const long long lpage = pos / args.page_tokens;
-                const int slot = static_cast<int>(pos - lpage * args.page_tokens);
-                const long long phys = args.block_table[lpage];
-                const size_t off =
-                    ((((static_cast<size_t>(phys) * args.n_layers + args.layer) * 2 + (region - 1)) *
-                          args.n_kv_heads + kvh) * args.page_tokens + slot) * static_cast<size_t>(hd);
-                dst = args.kv_pool + off;
-              }
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                st_global_v4(dst + j * 32 + q * 8, pack_bf16(o0[q * 8 + 0], o0[q * 8 + 1]),
-                             pack_bf16(o0[q * 8 + 2], o0[q * 8 + 3]), pack_bf16(o0[q * 8 + 4], o0[q * 8 + 5]),
-                             pack_bf16(o0[q * 8 + 6], o0[q * 8 + 7]));
-                st_global_v4(dst + half + j * 32 + q * 8, pack_bf16(o1[q * 8 + 0], o1[q * 8 + 1]),
-                             pack_bf16(o1[q * 8 + 2], o1[q * 8 + 3]), pack_bf16(o1[q * 8 + 4], o1[q * 8 + 5]),
-                             pack_bf16(o1[q * 8 + 6], o1[q * 8 + 7]));
-              }
-            }
-          }
-        }
+        gemm_epilogue<BLOCK_N, EPI>(args, tbase, row, m, n_blk, partial, blockIdx.x, first_part * cs + rank, n_parts,
+                                    cs, ep_tid);
       }
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
@@ -404,6 +463,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   __syncthreads();
+  if (cs > 1) cluster_sync();  // no peer may still multicast into this CTA's smem / barriers
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<Cfg::kTmemCols>(tmem_base);

@@ -1,0 +1,196 @@
+// 2-SM tcgen05 GEMM (cta_group::2): the projection GEMMs of a chunk with
+// more than 128 rows.
+//
+// A CTA pair (cluster of 2, one TPC) computes a 256 x 256 output tile: each
+// CTA TMA-loads its own 128 rows of A and 128 rows of the weight tile, the
+// leader issues tcgen05.mma.cta_group::2 (M = 256) that reads both CTAs'
+// shared memory, and each CTA receives its 128 output rows x 256 columns in
+// its own TMEM. Per SM that is 32 KB of operands per 64-deep k-block instead
+// of 48 KB for the 1-SM 128 x 256 tile: at M = 512 the projections are bound
+// by L2 -> SM bandwidth, so this is a 1.5x cut in the limiting resource.
+//
+// Pipeline (per pair): both producers wait on their own `empty` barrier,
+// load their halves and count the bytes on the LEADER's `full` barrier (peer
+// bit masked off); the leader's MMA thread waits `full`, issues 4 MMAs per
+// k-block, and multicasts the stage release to both CTAs' `empty`. The
+// accumulator handshake is the same across the pair: the leader's commit
+// multicasts `tmem_full` to both CTAs; both epilogues arrive on the leader's
+// `tmem_empty` (count 256). Split-K parts / stream-K partials are reduced per
+// CTA exactly like the 1-SM kernel (gemm_epilogue).
+#pragma once
+
+#include "gemm.cuh"
+
+namespace cake_dev {
+
+constexpr int kGemm2BlockN = 256;
+
+struct Gemm2Cfg {
+  static constexpr int kABytes = kGemmBlockM * kGemmBlockK * 2;            // this CTA's 128 rows of A
+  static constexpr int kBBytes = (kGemm2BlockN / 2) * kGemmBlockK * 2;     // this CTA's 128 rows of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (200 * 1024) / kStageBytes;               // 6
+  static constexpr int kTmemCols = 512;                                    // 2 x 256-column accumulators
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+};
+
+template <int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm2_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                    const GemmArgs args) {
+  using Cfg = Gemm2Cfg;
+  constexpr int kStages = Cfg::kStages;
+  constexpr int BLOCK_N = kGemm2BlockN;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ int s_abort;
+
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  // One abort decision per pair (a lone CTA leaving would strand its peer).
+  if (threadIdx.x == 0) s_abort = (args.abort_flag != nullptr) ? *(volatile const int*)args.abort_flag : 0;
+  cluster_sync();
+  const int abort_pair = ld_shared_cluster_s32(mapa_shared(smem_u32(&s_abort), 0));
+  if (abort_pair) {
+    cluster_sync();
+    return;
+  }
+
+  const uint32_t raw_base = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_base + 1023u) & ~1023u) - raw_base);
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + kStages * Cfg::kABytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages * Cfg::kStageBytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;  // [2]
+  uint64_t* tempty_bar = tfull_bar + 2;       // [2] (leader's copy is the live one)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x / 32;
+  const uint32_t lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 2 * 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_2sm<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int pair = blockIdx.x / 2;
+  const int n_pairs = gridDim.x / 2;
+  const int nk = args.num_k_blocks;
+  const int m_pairs = (args.num_m_blocks + 1) / 2;
+  const long long units = static_cast<long long>(m_pairs) * args.num_n_blocks * nk;
+  int tile, kb0, kb1;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer (both CTAs)
+      const uint64_t pol_w = policy_evict_last();
+      const uint64_t pol_a = policy_evict_last();
+      StreamK sk(units, nk, pair, n_pairs, args.whole_tiles);
+      int stage = 0;
+      uint32_t phase = 0;
+      while (sk.next(tile, kb0, kb1)) {
+        const int m_row = (tile % m_pairs) * 256 + static_cast<int>(rank) * 128;
+        const int n_row = (tile / m_pairs) * BLOCK_N + static_cast<int>(rank) * (BLOCK_N / 2);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1u);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
+          tma_load_2d_2sm(smem_a + stage * Cfg::kABytes, &tmap_a, &full_bar[stage], kb * kGemmBlockK, m_row, pol_a);
+          tma_load_2d_2sm(smem_b + stage * Cfg::kBBytes, &tmap_b, &full_bar[stage], kb * kGemmBlockK, n_row, pol_w);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ------------------------------------------------ MMA issuer (leader only)
+      constexpr uint32_t idesc = umma_idesc_bf16(256, BLOCK_N);
+      StreamK sk(units, nk, pair, n_pairs, args.whole_tiles);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      while (sk.next(tile, kb0, kb1)) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BLOCK_N);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem_a + stage * Cfg::kABytes);
+          const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kGemmBlockK / 16; ++k)
+            umma_bf16_ss_2sm(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32), idesc,
+                             (kb > kb0 || k > 0) ? 1u : 0u);
+          umma_commit_2sm_mc(&empty_bar[stage], 0x3);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        umma_commit_2sm_mc(&tfull_bar[acc], 0x3);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..5, both CTAs)
+    const int ew = warp & 3;
+    const int row = ew * 32 + static_cast<int>(lane);
+    const int ep_tid = threadIdx.x - 64;
+    const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    StreamK sk(units, nk, pair, n_pairs, args.whole_tiles);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    while (sk.next(tile, kb0, kb1)) {
+      const int m = (tile % m_pairs) * 256 + static_cast<int>(rank) * 128 + row;
+      const int n_blk = tile / m_pairs;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase =
+          tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * BLOCK_N);
+      const bool partial = kb0 > 0;
+      int first_part = 0, n_parts = 0;
+      if (!partial && kb1 < nk) {
+        const long long u_tile = static_cast<long long>(tile) * nk;
+        first_part = sk.cta_of(u_tile) + 1;
+        n_parts = sk.cta_of(u_tile + nk - 1) - first_part + 1;
+      }
+      gemm_epilogue<BLOCK_N, EPI>(args, tbase, row, m, n_blk, partial, blockIdx.x,
+                                  first_part * 2 + static_cast<int>(rank), n_parts, 2, ep_tid);
+      tc_fence_before();
+      mbar_arrive_cluster(leader_tempty0 + acc * 8);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  }
+
+  __syncthreads();
+  cluster_sync();  // the pair's MMAs / multicasts / remote arrives are all done
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace cake_dev

@@ -24,6 +24,9 @@ def gemm(a, b, c, epi, bn):
         raise RuntimeError(f"gemm status {st}: {err()}")
 
 
+sched = int(os.environ.get("GEMM_SCHED", "1"))
+lib.cake_gemm_set_schedule(sched)
+print("schedule", sched)
 torch.manual_seed(0)
 ok = True
 for (M, N, K) in [(128, 256, 64), (128, 128, 128), (200, 256, 512), (512, 6144, 4096), (300, 4096, 14336),
