@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -232,6 +233,7 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
       n = num_sms() / 2;
     }
     max_pairs = std::min(n, num_sms() / 2);
+    if (std::getenv("CAKE_DEBUG_GEMM")) std::fprintf(stderr, "gemm2: occupancy reports %d co-resident pairs\n", n);
     configured = true;
   }
   a.num_m_blocks = (a.M + kGemmBlockM - 1) / kGemmBlockM;
@@ -246,8 +248,11 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
     const long long units = static_cast<long long>(tiles) * a.num_k_blocks;
     pairs = static_cast<int>(std::max<long long>(1, std::min<long long>(max_pairs, units / 8)));
   } else {
+    // split parts run concurrently (the owner waits for its partner): keep
+    // tiles * split within the SM pairs so every part is resident together
+    const int pair_budget = num_sms() / 2;
     int split = 1;
-    while (tiles * (split + 1) <= max_pairs && a.num_k_blocks % (split + 1) == 0 &&
+    while (tiles * (split + 1) <= pair_budget && a.num_k_blocks % (split + 1) == 0 &&
            a.num_k_blocks / (split + 1) >= 8)
       ++split;
     a.whole_tiles = split == 1 ? 1 : 0;
@@ -261,7 +266,12 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
 
 int gemm_dispatch(int bn, int epi, const CUtensorMap& ta, const CUtensorMap* tb3, const GemmArgs& a,
                   cudaStream_t s) {
-  if (g_gemm_2sm && a.M > kGemmBlockM && a.N % kGemm2BlockN == 0 && (bn == 256 || epi != kEpiQkv)) {
+  // 2-SM tiles pay off when they alone fill most SM pairs (QKV: 48, gate/up: 224 at
+  // M = 512); few-tile projections (O, down: 32) stay on 1-SM 128 x 128 tiles,
+  // measured faster than 2-SM + split-K (tools/gemm_fixed_cost.py).
+  const int pair_tiles = ((a.M + 255) / 256) * (a.N / kGemm2BlockN);
+  if (g_gemm_2sm && a.M > kGemmBlockM && a.N % kGemm2BlockN == 0 && (bn == 256 || epi != kEpiQkv) &&
+      pair_tiles >= 40) {
     // B maps: index k holds box rows bn >> k; the 2-SM kernel loads 128-row halves
     const CUtensorMap& half = tb3[bn == 256 ? 1 : 0];
     switch (epi) {

@@ -131,16 +131,16 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t tba
   const bool valid = m < args.M;
   if (partial) {
     // ---- partial segment: publish the fp32 tile in this CTA's slot
-    float4* slot = reinterpret_cast<float4*>(args.sk_ws + (static_cast<size_t>(my_slot) * kGemmBlockM + row) * BLOCK_N);
+    // column-major slot [BLOCK_N][128]: for each column the warp's 32 rows are
+    // one coalesced 128-B line
+    float* slot = args.sk_ws + static_cast<size_t>(my_slot) * kGemmBlockM * BLOCK_N + row;
 #pragma unroll 1
     for (int c = 0; c < BLOCK_N / 32; ++c) {
       uint32_t r[32];
       tmem_ld32(tbase + c * 32, r);
       tmem_ld_wait();
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        slot[c * 8 + q] = make_float4(__uint_as_float(r[q * 4]), __uint_as_float(r[q * 4 + 1]),
-                                      __uint_as_float(r[q * 4 + 2]), __uint_as_float(r[q * 4 + 3]));
+      for (int i = 0; i < 32; ++i) __stcg(slot + (c * 32 + i) * kGemmBlockM, __uint_as_float(r[i]));
     }
     __threadfence();
     named_bar_sync(1, 128);
@@ -160,16 +160,10 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t tba
       tmem_ld32(tbase + col, r);
       tmem_ld_wait();
       for (int p = 0; p < n_parts; ++p) {
-        const float4* part = reinterpret_cast<const float4*>(
-            args.sk_ws + (static_cast<size_t>(first_slot + p * slot_stride) * kGemmBlockM + row) * BLOCK_N + col);
+        const float* part = args.sk_ws + static_cast<size_t>(first_slot + p * slot_stride) * kGemmBlockM * BLOCK_N +
+                            static_cast<size_t>(col) * kGemmBlockM + row;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 v = __ldcg(part + q);
-          r[q * 4] = __float_as_uint(__uint_as_float(r[q * 4]) + v.x);
-          r[q * 4 + 1] = __float_as_uint(__uint_as_float(r[q * 4 + 1]) + v.y);
-          r[q * 4 + 2] = __float_as_uint(__uint_as_float(r[q * 4 + 2]) + v.z);
-          r[q * 4 + 3] = __float_as_uint(__uint_as_float(r[q * 4 + 3]) + v.w);
-        }
+        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) + __ldcg(part + i * kGemmBlockM));
       }
     };
 
