@@ -15,8 +15,13 @@
 //                    MN-major SW128), O accumulator in TMEM
 // The running max is only moved (and O rescaled in TMEM) when it grows by
 // more than 2^8, so the common block costs no O round trip.
-// Roles (256 threads): warp 0 TMA producer, warp 1 TMEM owner + MMA issuer,
-// warps 4-7 softmax + epilogue (warp w%4 owns TMEM lanes 32*(w%4)..).
+// Q lives in TMEM (the A operand of QK^T, like P for PV), so each block's
+// MMAs read only K and V from shared memory.
+// Roles (384 threads): warp 0 TMA producer of K (3-stage ring, freed
+// right after each QK^T), warp 2 TMA producer of V (2-stage ring, freed after
+// each PV), warp 1 TMEM owner + MMA issuer, warps 4-11 softmax + epilogue in
+// two column groups (warp w%4 owns TMEM lanes 32*(w%4)..; two warps per
+// sub-partition hide the MUFU / TMEM-load latency of the row chains).
 #pragma once
 
 #include "attention.cuh"
@@ -26,7 +31,7 @@ namespace cake_dev {
 
 constexpr int kFaRows = 128;
 constexpr int kFaKeys = 128;  // two pages
-constexpr int kFaThreads = 256;
+constexpr int kFaThreads = 384;  // 4 role warps + 2 softmax groups of 4 warps
 
 template <int HD>
 struct FaCfg {
@@ -34,12 +39,16 @@ struct FaCfg {
   static constexpr int kTileBytes = kFaRows * HD * 2;        // Q / K / V tile (128 rows)
   static constexpr int kHalfBytes = kFaRows * 128;           // one 64-wide slice of a tile
   static constexpr int kPageHalfBytes = 64 * 128;            // one page x 64 elements
-  static constexpr int kSmem = 5 * kTileBytes + 1024 + 256;  // Q + 2 K + 2 V + align + barriers
+  static constexpr int kKStages = 3;                          // K released right after its QK^T
+  static constexpr int kVStages = 3;                          // V released after its PV
+  static constexpr int kSmem = (kKStages + kVStages) * kTileBytes + 1024 + 256;
   static constexpr uint32_t kTmemCols = 512;
-  static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO = 256;
+  // S double buffer, O accumulator, Q (bf16 pairs: HD/2 columns) as the TMEM A operand of QK^T
+  static constexpr uint32_t kColS0 = 0, kColS1 = 128, kColO = 256, kColQ = 384;
 };
 
 struct FaArgs {
+  const __nv_bfloat16* q;  // [C, n_q, hd] (rows read once, into TMEM)
   const int* block_table;
   __nv_bfloat16* out;     // [C, n_q, hd] (splits == 1)
   float* part_o;          // [splits, C*n_q, hd]
@@ -87,30 +96,35 @@ __global__ void __launch_bounds__(kFaThreads, 1)
 
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-  uint8_t* sQ = smem;
-  uint8_t* sK = smem + Cfg::kTileBytes;        // [2][tile]
-  uint8_t* sV = sK + 2 * Cfg::kTileBytes;      // [2][tile]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * Cfg::kTileBytes);
-  uint64_t* q_full = bar;
-  uint64_t* k_full = bar + 1;     // [2]
-  uint64_t* v_full = bar + 3;     // [2]
-  uint64_t* kv_empty = bar + 5;   // [2]
-  uint64_t* s_full = bar + 7;     // [2]
-  uint64_t* p_ready = bar + 9;    // [2]
-  uint64_t* pv_done = bar + 11;
-  uint64_t* o_final = bar + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+  uint8_t* sK = smem;                                       // [kKStages][tile]
+  uint8_t* sV = sK + Cfg::kKStages * Cfg::kTileBytes;      // [kVStages][tile]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + Cfg::kVStages * Cfg::kTileBytes);
+  uint64_t* q_ready = bar;        // Q rows stored into TMEM by the softmax warps
+  uint64_t* k_full = bar + 1;     // [3]
+  uint64_t* k_empty = bar + 4;    // [3]
+  uint64_t* v_full = bar + 7;     // [3]
+  uint64_t* v_empty = bar + 10;   // [3]
+  uint64_t* s_full = bar + 13;    // [2]
+  uint64_t* p_ready = bar + 15;   // [2]
+  uint64_t* pv_done = bar + 17;
+  uint64_t* o_final = bar + 18;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 19);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_kv);
-    mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    mbar_init(q_ready, 256);
+    for (int s = 0; s < Cfg::kKStages; ++s) {
       mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < Cfg::kVStages; ++s) {
       mbar_init(&v_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_ready[s], 128);
+      mbar_init(&p_ready[s], 256);
     }
     mbar_init(pv_done, 1);
     mbar_init(o_final, 1);
@@ -122,43 +136,44 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  const long long planes = static_cast<long long>(a.n_layers) * 2 * a.n_kv_heads;
+  auto page_row = [&](int lp, int kv) -> int32_t {  // first pool row of (page, layer, K|V, kv head)
+    const long long ph = a.block_table[lp];
+    return static_cast<int32_t>(((ph * planes) + (static_cast<long long>(a.layer) * 2 + kv) * a.n_kv_heads + kvh) * 64);
+  };
   if (warp == 0) {
     if (lane == 0 && nb > 0) {
-      // ------------------------------------------------ TMA producer
-      mbar_arrive_expect_tx(q_full, Cfg::kTileBytes);
-#pragma unroll
-      for (int h = 0; h < Cfg::kHalves; ++h) {
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(sQ + h * Cfg::kHalfBytes)),
-            "l"(reinterpret_cast<uint64_t>(&tm_q)), "r"(smem_u32(q_full)), "r"(h * 64), "r"(kvh * G), "r"(tok0)
-            : "memory");
-      }
-      const long long planes = static_cast<long long>(a.n_layers) * 2 * a.n_kv_heads;
+      // ------------------------------------------------ TMA producer: K blocks
       for (int j = 0; j < nb; ++j) {
-        const int s = j & 1;
-        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1u);
+        const int s = j % Cfg::kKStages;
+        mbar_wait(&k_empty[s], ((j / Cfg::kKStages) & 1) ^ 1u);
         const int lp0 = p_begin + 2 * j;
         const int lp1 = (lp0 + 1 < p_end) ? lp0 + 1 : lp0;  // odd tail: reload page 0 (its keys are masked)
-        const long long ph0 = a.block_table[lp0], ph1 = a.block_table[lp1];
-        const long long base_k0 = ((ph0 * planes) + (static_cast<long long>(a.layer) * 2 + 0) * a.n_kv_heads + kvh) * 64;
-        const long long base_k1 = ((ph1 * planes) + (static_cast<long long>(a.layer) * 2 + 0) * a.n_kv_heads + kvh) * 64;
-        const long long vstep = static_cast<long long>(a.n_kv_heads) * 64;  // K plane -> V plane
+        const int32_t r0 = page_row(lp0, 0), r1 = page_row(lp1, 0);
         mbar_arrive_expect_tx(&k_full[s], Cfg::kTileBytes);
 #pragma unroll
         for (int h = 0; h < Cfg::kHalves; ++h) {
-          tma_load_2d(sK + s * Cfg::kTileBytes + h * Cfg::kHalfBytes, &tm_kv, &k_full[s], h * 64,
-                      static_cast<int32_t>(base_k0));
+          tma_load_2d(sK + s * Cfg::kTileBytes + h * Cfg::kHalfBytes, &tm_kv, &k_full[s], h * 64, r0);
           tma_load_2d(sK + s * Cfg::kTileBytes + h * Cfg::kHalfBytes + Cfg::kPageHalfBytes, &tm_kv, &k_full[s],
-                      h * 64, static_cast<int32_t>(base_k1));
+                      h * 64, r1);
         }
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0 && nb > 0) {
+      // ------------------------------------------------ TMA producer: V blocks
+      for (int j = 0; j < nb; ++j) {
+        const int s = j % Cfg::kVStages;
+        mbar_wait(&v_empty[s], ((j / Cfg::kVStages) & 1) ^ 1u);
+        const int lp0 = p_begin + 2 * j;
+        const int lp1 = (lp0 + 1 < p_end) ? lp0 + 1 : lp0;
+        const int32_t r0 = page_row(lp0, 1), r1 = page_row(lp1, 1);
         mbar_arrive_expect_tx(&v_full[s], Cfg::kTileBytes);
 #pragma unroll
         for (int h = 0; h < Cfg::kHalves; ++h) {
-          tma_load_2d(sV + s * Cfg::kTileBytes + h * Cfg::kHalfBytes, &tm_kv, &v_full[s], h * 64,
-                      static_cast<int32_t>(base_k0 + vstep));
+          tma_load_2d(sV + s * Cfg::kTileBytes + h * Cfg::kHalfBytes, &tm_kv, &v_full[s], h * 64, r0);
           tma_load_2d(sV + s * Cfg::kTileBytes + h * Cfg::kHalfBytes + Cfg::kPageHalfBytes, &tm_kv, &v_full[s],
-                      h * 64, static_cast<int32_t>(base_k1 + vstep));
+                      h * 64, r1);
         }
       }
     }
@@ -167,42 +182,59 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       // ------------------------------------------------ MMA issuer
       constexpr uint32_t idesc_s = umma_idesc_bf16(kFaRows, kFaKeys, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(kFaRows, HD, false, true);
-      const uint32_t q_addr = smem_u32(sQ);
-      mbar_wait(q_full, 0);
+      mbar_wait(q_ready, 0);
+      tc_fence_after();
       auto issue_pv = [&](int jj) {
         const int s = jj & 1;
+        const int vs = jj % Cfg::kVStages;
         mbar_wait(&p_ready[s], (jj >> 1) & 1);
-        mbar_wait(&v_full[s], (jj >> 1) & 1);
+        mbar_wait(&v_full[vs], (jj / Cfg::kVStages) & 1);
         tc_fence_after();
-        const uint32_t v_addr = smem_u32(sV + s * Cfg::kTileBytes);
+        const uint32_t v_addr = smem_u32(sV + vs * Cfg::kTileBytes);
         const uint32_t p_col = tmem + (s ? Cfg::kColS1 : Cfg::kColS0);
 #pragma unroll
         for (int kk = 0; kk < kFaKeys / 16; ++kk) {
           const uint64_t bdesc = umma_desc_sw128_mn(v_addr + kk * 16 * 128, Cfg::kHalfBytes, 1024);
           umma_bf16_ts(tmem + Cfg::kColO, p_col + kk * 8, bdesc, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
         }
-        umma_commit(&kv_empty[s]);
+        umma_commit(&v_empty[vs]);
         umma_commit(pv_done);
       };
-      for (int j = 0; j < nb; ++j) {
-        const int s = j & 1;
-        mbar_wait(&k_full[s], (j >> 1) & 1);
+      auto issue_s = [&](int jj) {
+        const int s = jj & 1;
+        const int ks = jj % Cfg::kKStages;
+        mbar_wait(&k_full[ks], (jj / Cfg::kKStages) & 1);
         tc_fence_after();
-        const uint32_t k_addr = smem_u32(sK + s * Cfg::kTileBytes);
+        const uint32_t k_addr = smem_u32(sK + ks * Cfg::kTileBytes);
         const uint32_t d = tmem + (s ? Cfg::kColS1 : Cfg::kColS0);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * Cfg::kHalfBytes + (kk & 3) * 32;
-          umma_bf16_ss(d, umma_desc_sw128(q_addr + off), umma_desc_sw128(k_addr + off), idesc_s, kk > 0 ? 1u : 0u);
+          umma_bf16_ts(d, tmem + Cfg::kColQ + kk * 8, umma_desc_sw128(k_addr + off), idesc_s, kk > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[s]);
-        if (j >= 1) issue_pv(j - 1);
+        umma_commit(&k_empty[ks]);
+      };
+      // S(j+1) is issued BEFORE waiting for P(j): the tensor pipe computes the
+      // next block's scores while the softmax warps work on this one. (S(j+1)
+      // reuses the buffer of P(j-1), whose PV was issued earlier: in-order pipe.)
+      issue_s(0);
+      for (int j = 0; j < nb; ++j) {
+        if (j + 1 < nb) issue_s(j + 1);
+        issue_pv(j);
       }
-      issue_pv(nb - 1);
       umma_commit(o_final);
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ softmax + epilogue
+    // Two groups of 4 warps share the TMEM lanes (rows): group g owns score
+    // columns [64g, 64g+64), P columns [32g, 32g+32) and O columns
+    // [g*HD/2, (g+1)*HD/2). The row max is exchanged through shared memory
+    // once per block (double-buffered by block parity), the row sum once at
+    // the end, so both groups take identical rescale decisions.
+    __shared__ float xmax[2][2][kFaRows];
+    __shared__ float xsum[2][kFaRows];
+    const int g = (warp - 4) >> 2;
     const int q4 = warp & 3;
     const int row = q4 * 32 + static_cast<int>(lane);
     const int t = tok0 + row / G;
@@ -211,41 +243,70 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     const long long kmax_valid = static_cast<long long>(p_end) * kAttnPage;  // keys past the split are absent
     const long long qpos_min = a.chunk_start + tok0;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
+    constexpr int kHalfKeys = kFaKeys / 2;
+    constexpr int kOCols = HD / 2;
+    const float sc = a.scale_log2;
+    {
+      // this thread's Q row, half g (HD/2 bf16 = HD/4 packed columns), into TMEM
+      uint32_t qv[32];
+      const bool live = t < a.chunk_len && nb > 0;
+      const uint4* src = reinterpret_cast<const uint4*>(a.q + (static_cast<size_t>(t) * a.n_q_heads + head) * HD +
+                                                        g * (HD / 2));
+#pragma unroll
+      for (int i = 0; i < HD / 16; ++i) {
+        const uint4 v = live ? __ldg(src + i) : make_uint4(0u, 0u, 0u, 0u);
+        qv[4 * i] = v.x;
+        qv[4 * i + 1] = v.y;
+        qv[4 * i + 2] = v.z;
+        qv[4 * i + 3] = v.w;
+      }
+      if constexpr (HD == 128) {
+        tmem_st32(tmem + lane_off + Cfg::kColQ + g * 32, qv);
+      } else {
+        tmem_st16(tmem + lane_off + Cfg::kColQ + g * 16, qv);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(q_ready);
+    }
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < nb; ++j) {
       const int s = j & 1;
       mbar_wait(&s_full[s], (j >> 1) & 1);
       tc_fence_after();
       const uint32_t tS = tmem + lane_off + (s ? Cfg::kColS1 : Cfg::kColS0);
-      float sv[kFaKeys];
+      float sv[kHalfKeys];
 #pragma unroll
-      for (int c = 0; c < kFaKeys / 32; ++c) {
+      for (int c = 0; c < kHalfKeys / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(tS + c * 32, r);
+        tmem_ld32(tS + g * kHalfKeys + c * 32, r);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(r[i]) * a.scale_log2;
+        for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(r[i]);
       }
-      const long long kbase = static_cast<long long>(p_begin + 2 * j) * kAttnPage;
-      if (kbase + kFaKeys - 1 > qpos_min || kbase + kFaKeys > kmax_valid) {
+      const long long kbase = static_cast<long long>(p_begin + 2 * j) * kAttnPage + g * kHalfKeys;
+      if (kbase + kHalfKeys - 1 > qpos_min || kbase + kHalfKeys > kmax_valid) {
 #pragma unroll
-        for (int i = 0; i < kFaKeys; ++i) {
+        for (int i = 0; i < kHalfKeys; ++i) {
           const long long key = kbase + i;
           if (key > qpos || key >= kmax_valid) sv[i] = -INFINITY;
         }
       }
       float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < kFaKeys; ++i) mx = fmaxf(mx, sv[i]);
+      for (int i = 0; i < kHalfKeys; ++i) mx = fmaxf(mx, sv[i]);
+      xmax[s][g][row] = mx;
+      named_bar_sync(2, 256);
+      mx = fmaxf(xmax[s][0][row], xmax[s][1][row]) * sc;  // scale > 0: max commutes
       if (mx > m + 8.0f) {  // (also true on the first block with a visible key)
         if (m != -INFINITY) {
-          // move the reference max: O (all blocks < j, i.e. after PV(j-1)) and l scale by 2^(m - mx)
+          // move the reference max: O (blocks < j, i.e. after PV(j-1)) and l scale by 2^(m - mx)
           mbar_wait(pv_done, (j - 1) & 1);
           tc_fence_after();
           const float f = ex2_approx(m - mx);
-          const uint32_t tO = tmem + lane_off + Cfg::kColO;
+          const uint32_t tO = tmem + lane_off + Cfg::kColO + g * kOCols;
 #pragma unroll
-          for (int c = 0; c < HD / 32; ++c) {
+          for (int c = 0; c < kOCols / 32; ++c) {
             uint32_t r[32];
             tmem_ld32(tO + c * 32, r);
             tmem_ld_wait();
@@ -258,26 +319,27 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         }
         m = mx;
       }
-      const float base = (m == -INFINITY) ? 0.f : m;
-      float rs = 0.f;
+      const float nbase = (m == -INFINITY) ? 0.f : -m;
+      float rs0 = 0.f, rs1 = 0.f;
+      uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < kFaKeys / 64; ++c) {
-        uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float p0 = ex2_approx(sv[c * 64 + 2 * i] - base);
-          const float p1 = ex2_approx(sv[c * 64 + 2 * i + 1] - base);
-          rs += p0 + p1;
-          pk[i] = pack_bf16(p0, p1);
-        }
-        tmem_st32(tS + c * 32, pk);
+      for (int i = 0; i < 32; ++i) {
+        const float p0 = ex2_approx(fmaf(sv[2 * i], sc, nbase));
+        const float p1 = ex2_approx(fmaf(sv[2 * i + 1], sc, nbase));
+        rs0 += p0;
+        rs1 += p1;
+        pk[i] = pack_bf16(p0, p1);
       }
-      l += rs;
+      tmem_st32(tS + g * 32, pk);
+      l += rs0 + rs1;
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_ready[s]);
     }
-    // epilogue
+    // epilogue: total row sum, then this group's half of O
+    xsum[g][row] = l;
+    named_bar_sync(2, 256);
+    l = xsum[0][row] + xsum[1][row];
     const bool valid = t < a.chunk_len;
     const size_t orow = static_cast<size_t>(t) * a.n_q_heads + head;
     const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -285,9 +347,9 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       mbar_wait(o_final, 0);
       tc_fence_after();
     }
-    const uint32_t tO = tmem + lane_off + Cfg::kColO;
+    const uint32_t tO = tmem + lane_off + Cfg::kColO + g * kOCols;
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
+    for (int c = 0; c < kOCols / 32; ++c) {
       uint32_t r[32];
       if (nb > 0) {
         tmem_ld32(tO + c * 32, r);
@@ -297,8 +359,9 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         for (int i = 0; i < 32; ++i) r[i] = 0u;
       }
       if (!valid) continue;
+      const int col = g * kOCols + c * 32;
       if (a.num_splits == 1) {
-        __nv_bfloat16* dst = a.out + orow * HD + c * 32;
+        __nv_bfloat16* dst = a.out + orow * HD + col;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           st_global_v4(dst + q * 8, pack_bf16(__uint_as_float(r[q * 8]) * inv, __uint_as_float(r[q * 8 + 1]) * inv),
@@ -307,14 +370,14 @@ __global__ void __launch_bounds__(kFaThreads, 1)
                        pack_bf16(__uint_as_float(r[q * 8 + 6]) * inv, __uint_as_float(r[q * 8 + 7]) * inv));
       } else {
         const size_t rows = static_cast<size_t>(a.chunk_len) * a.n_q_heads;
-        float4* dst = reinterpret_cast<float4*>(a.part_o + (static_cast<size_t>(split) * rows + orow) * HD + c * 32);
+        float4* dst = reinterpret_cast<float4*>(a.part_o + (static_cast<size_t>(split) * rows + orow) * HD + col);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           dst[q] = make_float4(__uint_as_float(r[q * 4]) * inv, __uint_as_float(r[q * 4 + 1]) * inv,
                                __uint_as_float(r[q * 4 + 2]) * inv, __uint_as_float(r[q * 4 + 3]) * inv);
       }
     }
-    if (valid && a.num_splits > 1) {
+    if (valid && a.num_splits > 1 && g == 0) {
       const size_t rows = static_cast<size_t>(a.chunk_len) * a.n_q_heads;
       a.part_lse[static_cast<size_t>(split) * rows + orow] = l > 0.f ? m + __log2f(l) : -INFINITY;
     }

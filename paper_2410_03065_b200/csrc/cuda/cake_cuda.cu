@@ -484,6 +484,7 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
   dim3 grid(qtiles, m->nkv, splits);
   if (tc) {
     FaArgs fa;
+    fa.q = m->q;
     fa.block_table = bt;
     fa.out = m->attn;
     fa.part_o = m->part_o;
