@@ -27,6 +27,7 @@
 #include "cake/model.hpp"
 #include "cake/scheduler.hpp"
 #include "cake/store.hpp"
+#include "cake/tp.hpp"
 #include "cake/transfer.hpp"
 
 struct cake_model;
@@ -62,6 +63,7 @@ struct GpuOptions {
   int tp_rank = 0;
   int tp_size = 1;
   void* nccl_comm = nullptr;  // ncclComm_t when tp_size > 1
+  std::string tp_shm;         // POSIX shm name of the TP group's coordinator (cake/tp.hpp)
   int lookahead_layers = 3;   // claim the next chunk when this many layers of the current remain
   CostModel prior{5.0, 0.0002, 512};  // per-chunk duration prior (refine with calibrate())
   Micros race_margin_us = 200;        // race only when predicted to win by at least this
@@ -109,6 +111,7 @@ class GpuContext {
   std::vector<std::byte> read_chunk_kv(const ChunkSpec& chunk) const;
 
   const GpuRunInfo& last_run() const;
+  TpCoordinator* tp() const;  // non-null for tp_size > 1 with a coordinator
 
   struct Impl;
   Impl* impl() const { return impl_.get(); }

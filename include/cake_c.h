@@ -142,6 +142,7 @@ typedef struct cake_gpu_config {
   int lookahead_layers;
   int profile_kernels;
   int64_t race_margin_us;
+  const char* tp_shm; /* POSIX shm name of the TP group's coordinator (tp_size > 1), NULL otherwise */
 } cake_gpu_config;
 
 typedef struct cake_gpu_result {
@@ -182,6 +183,25 @@ CAKE_API int cake_gpu_set_profiling(cake_gpu* g, int mask);
 CAKE_API int cake_gpu_set_attention_impl(cake_gpu* g, int impl);
 CAKE_API void* cake_gpu_model(cake_gpu* g); /* cake_model* for direct C-ABI CUDA calls */
 CAKE_API void* cake_gpu_compute_stream(cake_gpu* g);
+
+/* ---- TP group coordination (cake/tp.hpp): leader publishes, followers mirror.
+ * Exposed so the host protocol can be tested (and driven) without a GPU.
+ * next_*: *has = 0 once the sequence ended. */
+typedef struct cake_tp cake_tp;
+CAKE_API int cake_tp_create(const char* shm_name, int rank, int size, cake_tp** out);
+CAKE_API int cake_tp_destroy(cake_tp* t);
+CAKE_API int cake_tp_begin_run(cake_tp* t, uint64_t run_id, uint32_t n_chunks);
+CAKE_API int cake_tp_end_run(cake_tp* t);
+CAKE_API int cake_tp_publish_compute(cake_tp* t, uint32_t chunk);
+CAKE_API int cake_tp_end_compute(cake_tp* t);
+CAKE_API int cake_tp_next_compute(cake_tp* t, uint32_t k, uint32_t* chunk, int* has);
+CAKE_API int cake_tp_publish_io(cake_tp* t, uint32_t chunk);
+CAKE_API int cake_tp_end_io(cake_tp* t);
+CAKE_API int cake_tp_next_io(cake_tp* t, uint32_t k, uint32_t* chunk, int* has);
+CAKE_API int cake_tp_shard_landed(cake_tp* t, uint32_t chunk);
+CAKE_API int cake_tp_wait_all_landed(cake_tp* t, uint32_t chunk);
+CAKE_API int cake_tp_publish_final(cake_tp* t, int recompute, int last_row);
+CAKE_API int cake_tp_wait_final(cake_tp* t, int* recompute, int* last_row);
 
 #ifdef __cplusplus
 }

@@ -121,6 +121,16 @@ CAKE_API int cake_model_get_info(const cake_model* m, cake_model_info* out);
  * product path), 1 = mma.sync flash attention (kept as an independent
  * cross-check in tests/test_gpu_kernels.py). */
 CAKE_API int cake_model_set_attention_impl(cake_model* m, int impl);
+/* NCCL plumbing for head-sharded TP (one process per GPU): rank 0 makes the
+ * 128-byte id, the launcher broadcasts it, every rank inits its communicator. */
+CAKE_API int cake_nccl_unique_id(void* out128);
+CAKE_API int cake_nccl_init(void** comm, const void* id128, int nranks, int rank);
+CAKE_API int cake_nccl_destroy(void* comm);
+/* Test driver: the n TP ranks' models (same device) run one chunk interleaved
+ * per half-layer, their row-parallel partials summed in rank order in place of
+ * the all-reduce. Verifies the sharding on a single GPU. */
+CAKE_API int cake_prefill_group(cake_model** models, int n, const int32_t* d_tokens, long long chunk_start,
+                                int chunk_len, const int32_t* d_block_table, void* stream);
 /* Attach an NCCL communicator (ncclComm_t) for tp_size > 1. */
 CAKE_API int cake_model_set_comm(cake_model* m, void* nccl_comm);
 

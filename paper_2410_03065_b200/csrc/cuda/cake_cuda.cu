@@ -357,6 +357,7 @@ struct cake_model {
   CUtensorMap tm_q, tm_kv;  // attention: Q rows of a GQA group, paged K/V pool
   int attn_impl = 0;        // 0 tcgen05 (product), 1 mma.sync (cross-check)
   ncclComm_t comm = nullptr;
+  bool emulated_tp = false;  // test driver sums the ranks' partials itself (cake_prefill_group)
   unsigned profile_mask = 0;  // bit k: bracket launches of kernel class k with events
   std::mutex prof_mu;  // launches come from the compute thread and the loader's pacer thread
   std::vector<ProfPair> prof;
@@ -677,13 +678,14 @@ int row_parallel(cake_model* m, int kind, const CUtensorMap& ta, const CUtensorM
     ProfScope ps(m, kind, s, flops, bytes);
     return gemm_dispatch(128, kEpiResid, ta, tb, g, s);
   }
-  if (!m->comm) return fail(CAKE_ESTATE, "tp_size > 1 but no NCCL communicator attached");
+  if (!m->comm && !m->emulated_tp) return fail(CAKE_ESTATE, "tp_size > 1 but no NCCL communicator attached");
   g.out = m->tp_buf;
   g.ldo = m->H;
   {
     ProfScope ps(m, kind, s, flops, bytes);
     CKS(gemm_dispatch(128, kEpiF32, ta, tb, g, s));
   }
+  if (m->emulated_tp) return CAKE_OK;  // partial stays in tp_buf for the group driver
   {
     ProfScope ps(m, CAKE_K_ALLREDUCE, s, 0.0, 4.0 * M * m->H);
     ncclResult_t r = ncclAllReduce(m->tp_buf, m->tp_buf, static_cast<size_t>(M) * m->H, ncclFloat32, ncclSum,
@@ -694,6 +696,58 @@ int row_parallel(cake_model* m, int kind, const CUtensorMap& ta, const CUtensorM
       m->h, m->tp_buf, static_cast<long long>(M) * m->H, abort_flag);
   CKL();
   return CAKE_OK;
+}
+
+}  // namespace
+
+namespace {
+
+int layer_attention_half(cake_model* m, int l, long long chunk_start, int M, const int32_t* d_block_table,
+                         const int32_t* d_abort, bool no_kv, cudaStream_t s) {
+  const int H = m->H;
+  LayerWeights& lw = m->layers[l];
+  CKS(rmsnorm(m, lw.ln1, 0, M, d_abort, s));
+  {
+    GemmArgs g{};
+    g.M = M;
+    g.N = no_kv ? m->nq * m->hd : m->qkv_rows;
+    g.K = H;
+    g.q_out = m->q;
+    g.kv_pool = m->pool;
+    g.block_table = d_block_table;
+    g.rope = m->rope;
+    g.pos0 = chunk_start;
+    g.n_q_heads = m->nq;
+    g.n_kv_heads = no_kv ? 0 : m->nkv;
+    g.head_dim = m->hd;
+    g.page_tokens = m->cfg.page_tokens;
+    g.layer = l;
+    g.n_layers = m->L;
+    g.abort_flag = d_abort;
+    if (g.N % m->bn_qkv) return fail(CAKE_EINVAL, "prefill: q-only pass needs tileable q rows");
+    ProfScope ps(m, CAKE_K_GEMM_QKV, s, 2.0 * M * g.N * H, 2.0 * g.N * H + 2.0 * M * H + 2.0 * M * g.N);
+    CKS(gemm_dispatch(m->bn_qkv, kEpiQkv, m->a_xn, lw.m_qkv, g, s));
+  }
+  CKS(attention(m, chunk_start, M, l, d_block_table, d_abort, s));
+  return row_parallel(m, CAKE_K_GEMM_O, m->a_attn, lw.m_o, m->nq * m->hd, M, d_abort, s);
+}
+
+int layer_mlp_half(cake_model* m, int l, int M, const int32_t* d_abort, cudaStream_t s) {
+  const int H = m->H;
+  LayerWeights& lw = m->layers[l];
+  CKS(rmsnorm(m, lw.ln2, 0, M, d_abort, s));
+  {
+    GemmArgs g{};
+    g.M = M;
+    g.N = 2 * m->F;
+    g.K = H;
+    g.out = m->act;
+    g.ldo = m->F;
+    g.abort_flag = d_abort;
+    ProfScope ps(m, CAKE_K_GEMM_GU, s, 2.0 * M * g.N * H, 2.0 * g.N * H + 2.0 * M * H + 2.0 * M * m->F);
+    CKS(gemm_dispatch(256, kEpiSwiglu, m->a_xn, lw.m_gu, g, s));
+  }
+  return row_parallel(m, CAKE_K_GEMM_D, m->a_act, lw.m_d, m->F, M, d_abort, s);
 }
 
 }  // namespace
@@ -1021,6 +1075,30 @@ int cake_model_get_info(const cake_model* m, cake_model_info* o) {
   return CAKE_OK;
 }
 
+int cake_nccl_unique_id(void* out128) {
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(CAKE_ENCCL + r, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  std::memcpy(out128, &id, sizeof(id));
+  return CAKE_OK;
+}
+
+int cake_nccl_init(void** comm, const void* id128, int nranks, int rank) {
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  ncclComm_t c;
+  ncclResult_t r = ncclCommInitRank(&c, nranks, id, rank);
+  if (r != ncclSuccess) return fail(CAKE_ENCCL + r, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  *comm = c;
+  return CAKE_OK;
+}
+
+int cake_nccl_destroy(void* comm) {
+  ncclResult_t r = ncclCommDestroy(static_cast<ncclComm_t>(comm));
+  if (r != ncclSuccess) return fail(CAKE_ENCCL + r, "ncclCommDestroy: %s", ncclGetErrorString(r));
+  return CAKE_OK;
+}
+
 int cake_model_set_attention_impl(cake_model* m, int impl) {
   if (impl != 0 && impl != 1) return fail(CAKE_EINVAL, "attention impl must be 0 (tcgen05) or 1 (mma.sync)");
   m->attn_impl = impl;
@@ -1093,46 +1171,48 @@ int cake_prefill_layers(cake_model* m, const int32_t* d_tokens, long long chunk_
   }
   const bool no_kv = (flags & CAKE_PREFILL_NO_KV_WRITE) != 0;
   for (int l = layer_begin; l < layer_end; ++l) {
-    LayerWeights& lw = m->layers[l];
-    CKS(rmsnorm(m, lw.ln1, 0, M, d_abort, s));
-    {
-      GemmArgs g{};
-      g.M = M;
-      g.N = no_kv ? m->nq * m->hd : m->qkv_rows;
-      g.K = H;
-      g.q_out = m->q;
-      g.kv_pool = m->pool;
-      g.block_table = d_block_table;
-      g.rope = m->rope;
-      g.pos0 = chunk_start;
-      g.n_q_heads = m->nq;
-      g.n_kv_heads = no_kv ? 0 : m->nkv;
-      g.head_dim = m->hd;
-      g.page_tokens = m->cfg.page_tokens;
-      g.layer = l;
-      g.n_layers = m->L;
-      g.abort_flag = d_abort;
-      if (g.N % m->bn_qkv) return fail(CAKE_EINVAL, "prefill: q-only pass needs tileable q rows");
-      ProfScope ps(m, CAKE_K_GEMM_QKV, s, 2.0 * M * g.N * H, 2.0 * g.N * H + 2.0 * M * H + 2.0 * M * g.N);
-      CKS(gemm_dispatch(m->bn_qkv, kEpiQkv, m->a_xn, lw.m_qkv, g, s));
-    }
-    CKS(attention(m, chunk_start, M, l, d_block_table, d_abort, s));
-    CKS(row_parallel(m, CAKE_K_GEMM_O, m->a_attn, lw.m_o, m->nq * m->hd, M, d_abort, s));
-    CKS(rmsnorm(m, lw.ln2, 0, M, d_abort, s));
-    {
-      GemmArgs g{};
-      g.M = M;
-      g.N = 2 * m->F;
-      g.K = H;
-      g.out = m->act;
-      g.ldo = m->F;
-      g.abort_flag = d_abort;
-      ProfScope ps(m, CAKE_K_GEMM_GU, s, 2.0 * M * g.N * H, 2.0 * g.N * H + 2.0 * M * H + 2.0 * M * m->F);
-      CKS(gemm_dispatch(256, kEpiSwiglu, m->a_xn, lw.m_gu, g, s));
-    }
-    CKS(row_parallel(m, CAKE_K_GEMM_D, m->a_act, lw.m_d, m->F, M, d_abort, s));
+    CKS(layer_attention_half(m, l, chunk_start, M, d_block_table, d_abort, no_kv, s));
+    CKS(layer_mlp_half(m, l, M, d_abort, s));
   }
   return CAKE_OK;
+}
+
+// Test driver of head-sharded tensor parallelism on ONE device: the ranks'
+// models run interleaved per half-layer on one stream and their row-parallel
+// partial sums are added in rank order (a deterministic stand-in for the
+// NCCL all-reduce the multi-GPU path calls at exactly the same two points).
+int cake_prefill_group(cake_model** models, int n, const int32_t* d_tokens, long long chunk_start, int chunk_len,
+                       const int32_t* d_block_table, void* stream) {
+  if (n < 1 || !models) return fail(CAKE_EINVAL, "group: no models");
+  cudaStream_t s = S(stream);
+  const int M = chunk_len;
+  for (int r = 0; r < n; ++r) {
+    cake_model* m = models[r];
+    if (m->cfg.tp_size != n || m->cfg.tp_rank != r) return fail(CAKE_EINVAL, "group: model %d is not rank %d of %d", r, r, n);
+    if (chunk_start % m->cfg.page_tokens || M < 1 || M > m->rows_cap) return fail(CAKE_EINVAL, "group: bad chunk");
+    m->emulated_tp = true;
+    embed_kernel<<<M, 128, 0, s>>>(d_tokens, m->embed, m->h, m->H, nullptr);
+    CKL();
+  }
+  auto reduce = [&]() -> int {
+    const long long cnt = static_cast<long long>(M) * models[0]->H;
+    for (int r = 0; r < n; ++r)
+      for (int q = 0; q < n; ++q) {
+        add_inplace_kernel<<<launch_grid_for(cnt / 4, 256), 256, 0, s>>>(models[r]->h, models[q]->tp_buf, cnt, nullptr);
+        CKL();
+      }
+    return CAKE_OK;
+  };
+  int st = CAKE_OK;
+  for (int l = 0; l < models[0]->L && st == CAKE_OK; ++l) {
+    for (int r = 0; r < n && st == CAKE_OK; ++r)
+      st = layer_attention_half(models[r], l, chunk_start, M, d_block_table, nullptr, false, s);
+    if (st == CAKE_OK) st = reduce();
+    for (int r = 0; r < n && st == CAKE_OK; ++r) st = layer_mlp_half(models[r], l, M, nullptr, s);
+    if (st == CAKE_OK) st = reduce();
+  }
+  for (int r = 0; r < n; ++r) models[r]->emulated_tp = false;
+  return st;
 }
 
 int cake_final_logits(cake_model* m, long long T, const int32_t* d_last_token, int recompute, int last_row,

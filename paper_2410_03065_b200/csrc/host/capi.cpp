@@ -3,6 +3,7 @@
 #include <functional>
 #include <memory>
 #include <string>
+#include <tuple>
 
 #include "cake/codec.hpp"
 #ifndef CAKE_REFERENCE_BUILD
@@ -378,6 +379,7 @@ int cake_gpu_create(const cake_gpu_config* c, cake_gpu** out) {
     if (c->lookahead_layers > 0) o.lookahead_layers = c->lookahead_layers;
     o.profile_kernels = c->profile_kernels != 0;
     if (c->race_margin_us > 0) o.race_margin_us = c->race_margin_us;
+    if (c->tp_shm) o.tp_shm = c->tp_shm;
     auto g = std::make_unique<cake_gpu>();
     g->ctx = std::make_unique<GpuContext>(m, o);
     *out = g.release();
@@ -483,6 +485,50 @@ int cake_gpu_set_attention_impl(cake_gpu* g, int impl) {
 
 void* cake_gpu_model(cake_gpu* g) { return g->ctx->model(); }
 void* cake_gpu_compute_stream(cake_gpu* g) { return g->ctx->compute_stream(); }
+
+struct cake_tp {
+  std::unique_ptr<TpCoordinator> c;
+};
+int cake_tp_create(const char* shm_name, int rank, int size, cake_tp** out) {
+  return guarded([&] {
+    if (!shm_name || !out) throw std::invalid_argument("tp: null argument");
+    auto t = std::make_unique<cake_tp>();
+    t->c = std::make_unique<TpCoordinator>(shm_name, rank, size);
+    *out = t.release();
+  });
+}
+int cake_tp_destroy(cake_tp* t) {
+  delete t;
+  return CAKE_OK;
+}
+int cake_tp_begin_run(cake_tp* t, uint64_t run_id, uint32_t n) { return guarded([&] { t->c->begin_run(run_id, n); }); }
+int cake_tp_end_run(cake_tp* t) { return guarded([&] { t->c->end_run(); }); }
+int cake_tp_publish_compute(cake_tp* t, uint32_t chunk) { return guarded([&] { t->c->publish_compute(chunk); }); }
+int cake_tp_end_compute(cake_tp* t) { return guarded([&] { t->c->end_compute(); }); }
+int cake_tp_next_compute(cake_tp* t, uint32_t k, uint32_t* chunk, int* has) {
+  return guarded([&] {
+    const auto v = t->c->next_compute(k);
+    *has = v ? 1 : 0;
+    *chunk = v.value_or(0);
+  });
+}
+int cake_tp_publish_io(cake_tp* t, uint32_t chunk) { return guarded([&] { t->c->publish_io(chunk); }); }
+int cake_tp_end_io(cake_tp* t) { return guarded([&] { t->c->end_io(); }); }
+int cake_tp_next_io(cake_tp* t, uint32_t k, uint32_t* chunk, int* has) {
+  return guarded([&] {
+    const auto v = t->c->next_io(k);
+    *has = v ? 1 : 0;
+    *chunk = v.value_or(0);
+  });
+}
+int cake_tp_shard_landed(cake_tp* t, uint32_t chunk) { return guarded([&] { t->c->shard_landed(chunk); }); }
+int cake_tp_wait_all_landed(cake_tp* t, uint32_t chunk) { return guarded([&] { t->c->wait_all_landed(chunk); }); }
+int cake_tp_publish_final(cake_tp* t, int recompute, int last_row) {
+  return guarded([&] { t->c->publish_final(recompute, last_row); });
+}
+int cake_tp_wait_final(cake_tp* t, int* recompute, int* last_row) {
+  return guarded([&] { std::tie(*recompute, *last_row) = t->c->wait_final(); });
+}
 #endif  // CAKE_REFERENCE_BUILD
 
 }  // extern "C"

@@ -118,6 +118,8 @@ struct GpuContext::Impl {
   std::vector<std::unique_ptr<Event>> ev_start, ev_near, ev_end, ev_io;
   std::unique_ptr<Event> ev_anchor, ev_copy_done, ev_final_start, ev_logits;  // created after set_device
   GpuRunInfo last;
+  std::unique_ptr<TpCoordinator> tp;
+  std::uint64_t run_counter = 0;
 
   void ensure_events(std::size_t n) {
     for (auto* v : {&ev_start, &ev_near, &ev_end, &ev_io})
@@ -158,10 +160,12 @@ GpuContext::GpuContext(const GpuModelConfig& cfg, const GpuOptions& opt) : impl_
   g.ev_logits = std::make_unique<Event>();
   check(cake_model_create(&mc, &g.model), "model create");
   check(cake_model_get_info(g.model, &g.info), "model info");
-  if (opt.tp_size > 1) {
-    if (!opt.nccl_comm) throw std::invalid_argument("gpu: tp_size > 1 needs an NCCL communicator");
-    check(cake_model_set_comm(g.model, opt.nccl_comm), "set comm");
-  }
+  // tp_size > 1 without a communicator is allowed for the single-device
+  // group driver (cake_prefill_group); a live run then fails loudly in the
+  // first row-parallel projection.
+  if (opt.tp_size > 1 && opt.nccl_comm) check(cake_model_set_comm(g.model, opt.nccl_comm), "set comm");
+  if (opt.tp_size > 1 && !opt.tp_shm.empty())
+    g.tp = std::make_unique<TpCoordinator>(opt.tp_shm, opt.tp_rank, opt.tp_size);
   check(cake_model_set_profiling(g.model, opt.profile_kernels ? -1 : 0), "profiling");
   check(cake_stream_create(&g.s_compute, 0), "stream");
   check(cake_stream_create(&g.s_copy, 1), "stream");     // loader work jumps the queue for free SMs
@@ -207,6 +211,7 @@ std::uint64_t GpuContext::kv_bytes_per_token() const {
 }
 int GpuContext::page_tokens() const { return impl_->cfg.page_tokens; }
 const GpuRunInfo& GpuContext::last_run() const { return impl_->last; }
+TpCoordinator* GpuContext::tp() const { return impl_->tp.get(); }
 
 namespace {
 
@@ -344,6 +349,7 @@ struct LiveRun {
   std::atomic<int> race_chunk{-1};
   std::atomic<int> racer{-1};  // kByCompute / kByIo
   TransferEngine* loader = nullptr;
+  TpCoordinator* tp = nullptr;  // leader side of a TP group (followers run run_follower)
   std::mutex commit_mu;
   std::condition_variable commit_cv;
   std::uint32_t n_committed = 0;
@@ -414,6 +420,7 @@ class GpuPrefillBackend final : public PrefillBackend {
 
   void launch(const ChunkSpec& c, bool contested) override {
     GpuContext::Impl& g = r_.g;
+    if (r_.tp) r_.tp->publish_compute(c.index);  // followers enqueue the same chunk (NCCL lockstep)
     const Micros predicted = predict_finish(c);
     if (contested) r_.start_race(c, kByCompute, g.s_compute);
     const std::int32_t* bt = r_.table_for(c.index, kByCompute);
@@ -502,6 +509,7 @@ class GpuLoaderSink final : public ChunkSink {
 
   void begin_chunk(const FetchTask& t) override {
     GpuContext::Impl& g = r_.g;
+    if (r_.tp) r_.tp->publish_io(t.chunk.index);  // every rank loads its shard of this chunk
     if (t.contested) r_.start_race(t.chunk, kByIo, g.s_copy);
     buf_ = g.staging[parity_].p;
     parity_ ^= 1;
@@ -522,6 +530,10 @@ class GpuLoaderSink final : public ChunkSink {
 
   Micros wait_chunk(const FetchTask& t) override {
     check(cake_event_sync(r_.g.ev_io[t.chunk.index]->h), "io wait");
+    if (r_.tp) {  // resident only when every rank's KV-head shard landed
+      r_.tp->shard_landed(t.chunk.index);
+      r_.tp->wait_all_landed(t.chunk.index);
+    }
     if (!r_.try_commit(t.chunk.index, kByIo)) return -1;  // compute landed it first
     r_.abort_compute(t.chunk.index);  // stop any compute work still queued for it
     return r_.device_time(r_.g.ev_io[t.chunk.index]->h);
@@ -542,6 +554,110 @@ class GpuLoaderSink final : public ChunkSink {
 
 }  // namespace
 
+// A TP follower mirrors the leader's decisions (cake/tp.hpp): it enqueues the
+// compute chunks the leader launched, loads its own KV-head shard of the
+// chunks the leader's loader claimed (same throttle, its own emulated link),
+// and joins the first-token step. Its collectives pair with the leader's.
+RunReport run_follower(GpuContext::Impl& g, TpCoordinator& tp, const RunPlan& plan,
+                       const std::vector<std::uint32_t>& tokens, const BandwidthTrace& trace, const ChunkStore& store,
+                       RunMode mode, const RunOptions& opt) {
+  const auto n = static_cast<std::uint32_t>(plan.chunks.size());
+  g.ensure_events(n);
+  tp.begin_run(++g.run_counter, n);
+  check(cake_cuda_device_sync(), "pre-run sync");
+  RunTimer timer;
+  check(cake_event_record(g.ev_anchor->h, g.s_compute), "anchor");
+  const Micros t0 = timer.now_us();
+  check(cake_stream_wait_event(g.s_copy, g.ev_anchor->h), "order");
+  check(cake_memset_async(g.abort_flags.p, 0, g.n_pages * sizeof(std::int32_t), g.s_compute), "abort reset");
+  upload_tokens(g, tokens, g.s_compute);
+  auto dev_time = [&](void* ev) {
+    float ms = 0.f;
+    check(cake_event_elapsed_ms(g.ev_anchor->h, ev, &ms), "elapsed");
+    return t0 + static_cast<Micros>(std::llround(ms * 1000.0));
+  };
+  std::vector<std::uint32_t> io_chunks;
+  std::exception_ptr io_error;
+  std::thread io([&] {
+    try {
+      const std::uint64_t quantum = std::max<std::uint64_t>(opt.throttle_quantum_bytes, 1);
+      Micros budget = 0;
+      for (std::uint32_t k = 0;; ++k) {
+        const auto c = tp.next_io(k);
+        if (!c) break;
+        const std::uint32_t i = *c;
+        const std::uint64_t total = plan.encoded_bytes[i];
+        ChunkReader rd = store.open_reader(plan.keys[i]);
+        std::vector<std::byte> host;  // file tier: read whole chunk (memory tier: zero-copy view)
+        const std::byte* src = nullptr;
+        if (rd.in_memory()) {
+          src = rd.view_next(static_cast<std::size_t>(total)).data();
+        } else {
+          host.resize(static_cast<std::size_t>(total));
+          if (rd.read(host) != host.size()) throw CorruptChunkError("tp follower: short read");
+          src = host.data();
+        }
+        std::byte* buf = g.staging[k & 1].p;
+        for (std::uint64_t off = 0; off < total;) {
+          const std::uint64_t len = std::min(quantum, total - off);
+          const Micros gate = budget + time_to_transfer_bits(trace, len * 8, budget);
+          timer.sleep_until_us_precise(gate);
+          check(cake_h2d_async(buf + off, src + off, len, g.s_copy), "slice H2D");
+          off += len;
+          budget = gate;
+          const Micros now = timer.now_us();
+          const Micros one = time_to_transfer_bits(trace, quantum * 8, budget);
+          if (budget + one < now) budget = now - one;
+        }
+        check(cake_kv_scatter(g.model, buf, static_cast<long long>(plan.chunks[i].token_start),
+                              static_cast<int>(plan.chunks[i].token_count), g.bt_primary.p, 0,
+                              static_cast<long long>(total), g.s_copy),
+              "scatter");
+        check(cake_event_record(g.ev_io[i]->h, g.s_copy), "record");
+        check(cake_event_sync(g.ev_io[i]->h), "io wait");
+        tp.shard_landed(i);
+        io_chunks.push_back(i);
+      }
+    } catch (...) {
+      io_error = std::current_exception();
+    }
+  });
+  std::vector<std::uint32_t> computed;
+  for (std::uint32_t k = 0;; ++k) {
+    const auto c = tp.next_compute(k);
+    if (!c) break;
+    const ChunkSpec& ch = plan.chunks[*c];
+    check(cake_event_record(g.ev_start[ch.index]->h, g.s_compute), "record");
+    check(cake_prefill_chunk(g.model, g.tokens.p + ch.token_start, static_cast<long long>(ch.token_start),
+                             static_cast<int>(ch.token_count), g.bt_primary.p, nullptr, 0, g.s_compute),
+          "prefill");
+    check(cake_event_record(g.ev_end[ch.index]->h, g.s_compute), "record");
+    computed.push_back(ch.index);
+  }
+  const auto [recompute, last_row] = tp.wait_final();
+  io.join();
+  if (io_error) std::rethrow_exception(io_error);
+  const ChunkSpec& tail = plan.chunks[n - 1];
+  const long long T = static_cast<long long>(tail.token_start + tail.token_count);
+  check(cake_final_logits(g.model, T, g.tokens.p + (T - 1), recompute, last_row, g.bt_primary.p, g.logits.p,
+                          g.s_compute),
+        "final logits");
+  check(cake_stream_sync(g.s_compute), "sync");
+  RunReport rep;
+  rep.mode = mode;
+  rep.n_chunks = n;
+  for (std::uint32_t i : computed)
+    rep.chunks.push_back({i, Side::compute, dev_time(g.ev_start[i]->h), dev_time(g.ev_end[i]->h), 0});
+  for (std::uint32_t i : io_chunks)
+    rep.chunks.push_back({i, Side::io, 0, dev_time(g.ev_io[i]->h), plan.encoded_bytes[i]});
+  detail::finalize_report(rep, 0);
+  rep.merge_point = detail::merge_from_records(rep);
+  rep.computed_fraction = static_cast<double>(rep.merge_point) / n;
+  g.final_bt = g.bt_primary.p;
+  tp.end_run();
+  return rep;
+}
+
 namespace detail {
 
 RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& tokens, const CostModel& cost,
@@ -557,8 +673,11 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   const bool io_on = mode == RunMode::io_only || (mode == RunMode::cake && opt.io_enabled);
   const bool compute_on = mode == RunMode::compute_only || (mode == RunMode::cake && opt.compute_enabled);
   if (!io_on && !compute_on) throw std::invalid_argument("run: no side enabled");
-  const bool race = opt.race_to_finish && io_on && compute_on;
+  TpCoordinator* tp = g.tp.get();
+  if (tp && !tp->leader()) return run_follower(g, *tp, plan, tokens, trace, store, mode, opt);
+  const bool race = opt.race_to_finish && io_on && compute_on && tp == nullptr;  // TP: boundary race not mirrored yet
   g.ensure_events(n);
+  if (tp) tp->begin_run(++g.run_counter, n);
   check(cake_cuda_device_sync(), "pre-run sync");
   long long launches0 = 0;
   check(cake_model_launch_count(g.model, &launches0, 1), "launch count");
@@ -566,6 +685,7 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   // ---------------------------------------------------------------- t = 0
   RunTimer timer;
   LiveRun run(g, plan, timer);
+  run.tp = tp;
   check(cake_event_record(g.ev_anchor->h, g.s_compute), "anchor");
   run.t0 = timer.now_us();
   check(cake_stream_wait_event(g.s_copy, g.ev_anchor->h), "order");
@@ -623,9 +743,11 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
     auto recs = engine.run_forward(plan.chunks, plan.keys, hooks);
     rep.chunks.insert(rep.chunks.end(), recs.begin(), recs.end());
   }
+  if (tp) tp->end_compute();
   // The first token needs every chunk committed, not the loader's threads
   // drained (a pacer may still be winding down a chunk it lost).
   run.wait_all_committed();
+  if (tp) tp->end_io();
   if (run.n_committed < n && loader) loader->wait();  // surfaces the loader's error, if any
   if (run.n_committed < n) throw std::logic_error("run: chunk coverage is incomplete");
 
@@ -641,6 +763,7 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   const ChunkSpec& tail = plan.chunks[n - 1];
   const bool tail_hidden = run.commit[n - 1].load() == kByCompute && backend.last_launched() == static_cast<int>(n - 1);
   const long long T = static_cast<long long>(tail.token_start + tail.token_count);
+  if (tp) tp->publish_final(tail_hidden ? 0 : 1, static_cast<int>(tail.token_count) - 1);
   check(cake_event_record(g.ev_final_start->h, g.s_compute), "record");
   check(cake_final_logits(g.model, T, g.tokens.p + (T - 1), tail_hidden ? 0 : 1, static_cast<int>(tail.token_count) - 1,
                           g.final_bt, g.logits.p, g.s_compute),
@@ -677,6 +800,7 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
                          (info.race_winner == 0 ? "compute" : "io"));
   rep.events.push_back("first token at " + std::to_string(info.first_token_us) + "us");
   g.last = std::move(info);
+  if (tp) tp->end_run();
   return rep;
 }
 

@@ -46,7 +46,7 @@ class CakeGpuConfig(C.Structure):
                 ("rms_eps", C.c_float), ("max_chunk", C.c_int), ("max_tokens", C.c_longlong),
                 ("weight_seed", C.c_ulonglong), ("device", C.c_int), ("tp_rank", C.c_int), ("tp_size", C.c_int),
                 ("nccl_comm", vp), ("lookahead_layers", C.c_int), ("profile_kernels", C.c_int),
-                ("race_margin_us", i64)]
+                ("race_margin_us", i64), ("tp_shm", C.c_char_p)]
 
 
 class CakeGpuResult(C.Structure):
@@ -106,6 +106,20 @@ _SIGS = {
     "cake_gpu_set_attention_impl": (C.c_int, [vp, C.c_int]),
     "cake_gpu_model": (vp, [vp]),
     "cake_gpu_compute_stream": (vp, [vp]),
+    "cake_tp_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, P(vp)]),
+    "cake_tp_destroy": (C.c_int, [vp]),
+    "cake_tp_begin_run": (C.c_int, [vp, u64, u32]),
+    "cake_tp_end_run": (C.c_int, [vp]),
+    "cake_tp_publish_compute": (C.c_int, [vp, u32]),
+    "cake_tp_end_compute": (C.c_int, [vp]),
+    "cake_tp_next_compute": (C.c_int, [vp, u32, P(u32), P(C.c_int)]),
+    "cake_tp_publish_io": (C.c_int, [vp, u32]),
+    "cake_tp_end_io": (C.c_int, [vp]),
+    "cake_tp_next_io": (C.c_int, [vp, u32, P(u32), P(C.c_int)]),
+    "cake_tp_shard_landed": (C.c_int, [vp, u32]),
+    "cake_tp_wait_all_landed": (C.c_int, [vp, u32]),
+    "cake_tp_publish_final": (C.c_int, [vp, C.c_int, C.c_int]),
+    "cake_tp_wait_final": (C.c_int, [vp, P(C.c_int), P(C.c_int)]),
 }
 
 
@@ -185,6 +199,10 @@ def load_cuda():
     lib.cake_kv_chunk_bytes.argtypes = [vp, C.c_int]
     lib.cake_kv_scatter.argtypes = [vp, vp, C.c_longlong, C.c_int, vp, C.c_longlong, C.c_longlong, vp]
     lib.cake_kv_gather.argtypes = [vp, vp, C.c_longlong, C.c_int, vp, vp]
+    lib.cake_prefill_group.argtypes = [C.POINTER(vp), C.c_int, vp, C.c_longlong, C.c_int, vp, vp]
+    lib.cake_final_logits.argtypes = [vp, C.c_longlong, vp, C.c_int, C.c_int, vp, vp, vp]
+    lib.cake_nccl_unique_id.argtypes = [vp]
+    lib.cake_nccl_init.argtypes = [C.POINTER(vp), vp, C.c_int, C.c_int]
     return lib
 
 
