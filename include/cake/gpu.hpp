@@ -23,6 +23,7 @@
 #include <string>
 #include <vector>
 
+#include "cake/codec.hpp"
 #include "cake/compute.hpp"
 #include "cake/model.hpp"
 #include "cake/scheduler.hpp"
@@ -104,7 +105,10 @@ class GpuContext {
 
   // Cache tier: compute-only pass over the seeded prompt, every chunk's KV
   // gathered to the tier format and put under its chain key.
-  PopulateResult build_cache_tier(ChunkStore& store, const RequestSpec& request, std::uint64_t prompt_seed);
+  // quant8: the chunk is encoded on the GPU (cake_kv_encode_q8), format of
+  // the reference's Codec::quant8 (codec.cpp:114-162) over the bf16 KV.
+  PopulateResult build_cache_tier(ChunkStore& store, const RequestSpec& request, std::uint64_t prompt_seed,
+                                  const Codec& codec = Codec::identity());
   // Compute-only pass timed per chunk with events; least-squares alpha/beta.
   CostModel calibrate(const RequestSpec& request, std::uint64_t prompt_seed);
   // Assembled cache of the last run (committed pages), tier format.

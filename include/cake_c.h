@@ -168,6 +168,9 @@ CAKE_API int cake_gpu_kv_bytes_per_token(const cake_gpu* g, uint64_t* out);
 /* Fill `store` (create it memory-resident+pinned) from a compute-only GPU pass. */
 CAKE_API int cake_gpu_build_tier(cake_gpu* g, cake_store* store, uint64_t total_tokens, uint32_t chunk_size,
                                  uint64_t prompt_seed);
+/* Cache-tier codec for build_tier and run: "identity" (default) or "quant8"
+ * (reference codec.cpp:114-162; decode fused into the GPU scatter). */
+CAKE_API int cake_gpu_set_codec(cake_gpu* g, const char* codec_id);
 CAKE_API int cake_gpu_calibrate(cake_gpu* g, uint64_t total_tokens, uint32_t chunk_size, uint64_t prompt_seed,
                                 double* alpha_ms, double* beta_ms_per_token);
 CAKE_API int cake_gpu_run(cake_gpu* g, cake_store* store, uint64_t total_tokens, uint32_t chunk_size,

@@ -171,6 +171,15 @@ CAKE_API int cake_kv_scatter(cake_model* m, const void* d_staging, long long chu
 /* Inverse: paged pool -> staging (cache-tier format). */
 CAKE_API int cake_kv_gather(cake_model* m, void* d_staging, long long chunk_start, int chunk_len,
                    const int32_t* d_block_table, void* stream);
+/* quant8 cache tier (reference proj/src/codec.cpp:114-162, Codec::quant8):
+ * encoded chunk = [lo fp16][hi fp16][one u8 level per element of the tier
+ * format], i.e. cake_kv_chunk_bytes/2 + 4 bytes. The decode is fused into the
+ * scatter (dequantise + permute into the bf16 pages, one pass); d_encoded + 4
+ * must be 16-B aligned. encode: a gathered bf16 chunk -> encoded (4-B aligned). */
+CAKE_API long long cake_kv_q8_bytes(const cake_model* m, int chunk_len);
+CAKE_API int cake_kv_scatter_q8(cake_model* m, const void* d_encoded, long long chunk_start, int chunk_len,
+                                const int32_t* d_block_table, void* stream);
+CAKE_API int cake_kv_encode_q8(cake_model* m, const void* d_chunk, int chunk_len, void* d_encoded, void* stream);
 
 /* ---------------------------------------------------------- profiling */
 enum {

@@ -353,6 +353,7 @@ struct cake_model {
   int max_splits = 16;
   size_t part_rows_cap = 0;  // splits * chunk rows * local q heads the partials hold
   float* tp_buf = nullptr;  // fp32 partial sums for the TP all-reduce
+  unsigned* q8_ws = nullptr;  // quant8 encode: ordered min/max keys
   CUtensorMap a_xn, a_attn, a_act;
   CUtensorMap tm_q, tm_kv;  // attention: Q rows of a GQA group, paged K/V pool
   int attn_impl = 0;        // 0 tcgen05 (product), 1 mma.sync (cross-check)
@@ -887,7 +888,7 @@ int cake_model_destroy(cake_model* m) {
                   static_cast<void*>(m->rope), static_cast<void*>(m->h), static_cast<void*>(m->xn),
                   static_cast<void*>(m->q), static_cast<void*>(m->attn), static_cast<void*>(m->act),
                   static_cast<void*>(m->part_o), static_cast<void*>(m->part_lse),
-                  static_cast<void*>(m->tp_buf)})
+                  static_cast<void*>(m->tp_buf), static_cast<void*>(m->q8_ws)})
     if (p) cudaFree(p);
   for (auto& p : m->prof) {
     cudaEventDestroy(p.a);
@@ -1040,6 +1041,7 @@ int cake_model_create(const cake_model_config* cfg, cake_model** out) {
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->part_lse), m->part_rows_cap * sizeof(float)))) return bail(st);
   if (c.tp_size > 1 && (st = alloc_dev(reinterpret_cast<void**>(&m->tp_buf), R * H * sizeof(float))))
     return bail(st);
+  if ((st = alloc_dev(reinterpret_cast<void**>(&m->q8_ws), 2 * sizeof(unsigned)))) return bail(st);
   cudaMemset(m->xn, 0, R * H * sizeof(bf16));
   cudaMemset(m->attn, 0, R * m->nq * hd * sizeof(bf16));
   cudaMemset(m->act, 0, R * F * sizeof(bf16));
@@ -1275,6 +1277,44 @@ int cake_kv_gather(cake_model* m, void* d_staging, long long chunk_start, int ch
                    const int32_t* d_block_table, void* stream) {
   return kv_permute(m, d_staging, chunk_start, chunk_len, d_block_table, 0, cake_kv_chunk_bytes(m, chunk_len),
                     false, S(stream));
+}
+
+long long cake_kv_q8_bytes(const cake_model* m, int chunk_len) { return cake_kv_chunk_bytes(m, chunk_len) / 2 + 4; }
+
+int cake_kv_scatter_q8(cake_model* m, const void* d_encoded, long long chunk_start, int chunk_len,
+                       const int32_t* d_block_table, void* stream) {
+  if (chunk_start % m->cfg.page_tokens) return fail(CAKE_EINVAL, "kv q8: chunk must start on a page boundary");
+  if ((reinterpret_cast<uintptr_t>(d_encoded) + 4) % 16)
+    return fail(CAKE_EINVAL, "kv q8: payload (encoded + 4) must be 16-B aligned");
+  const long long n = cake_kv_chunk_bytes(m, chunk_len) / 2;
+  KvLayout L{m->L, m->nkv, m->hd, m->cfg.page_tokens};
+  const unsigned n16 = static_cast<unsigned>(n / 16);
+  const int grid = launch_grid_for(n16, 256);
+  cudaStream_t s = S(stream);
+  ProfScope ps(m, CAKE_K_SCATTER, s, 0.0, static_cast<double>(n) + 2.0 * n);
+  const auto* enc = static_cast<const uint8_t*>(d_encoded);
+  kv_scatter_q8_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const uint4*>(enc + 4), reinterpret_cast<const __half*>(enc),
+                                            reinterpret_cast<uint4*>(m->pool), d_block_table,
+                                            chunk_start / m->cfg.page_tokens, chunk_len, L, n16);
+  CKL();
+  return CAKE_OK;
+}
+
+int cake_kv_encode_q8(cake_model* m, const void* d_chunk, int chunk_len, void* d_encoded, void* stream) {
+  if (reinterpret_cast<uintptr_t>(d_chunk) % 16 || reinterpret_cast<uintptr_t>(d_encoded) % 4)
+    return fail(CAKE_EINVAL, "kv q8 encode: chunk 16-B / encoded 4-B alignment");
+  const long long n = cake_kv_chunk_bytes(m, chunk_len) / 2;
+  const unsigned n8 = static_cast<unsigned>(n / 8);
+  cudaStream_t s = S(stream);
+  const unsigned init[2] = {0xFFFFFFFFu, 0u};
+  CK(cudaMemcpyAsync(m->q8_ws, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  const int grid = launch_grid_for(n8, 256);
+  kv_minmax_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(d_chunk), n8, m->q8_ws);
+  CKL();
+  kv_quant8_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(d_chunk), n8, m->q8_ws,
+                                        static_cast<uint8_t*>(d_encoded));
+  CKL();
+  return CAKE_OK;
 }
 
 int cake_gemm_set_schedule(int schedule) {

@@ -222,4 +222,118 @@ __global__ void kv_permute_kernel(uint4* __restrict__ staging, uint4* __restrict
   }
 }
 
+// ------------------------------------------------------------ quant8 tier codec
+// The reference's quant8 (proj/src/codec.cpp:114-162): one (lo, hi) fp16 pair
+// per chunk, then one byte per element, level = round((v - lo) / span * 255),
+// decode lo + q / 255 * span. Here the elements are the KV cache's bf16 values
+// (the reference's synthetic payload is fp16); arithmetic order and rounding
+// follow the reference op for op (explicit _rn intrinsics: no FMA contraction),
+// decode rounds to bf16 instead of fp16. Encoded chunk: [lo fp16][hi fp16][q u8 x n].
+__device__ __forceinline__ unsigned long long kv_pool_vec(unsigned v, const int* __restrict__ block_table,
+                                                          long long first_page, int chunk_len, const KvLayout& L) {
+  const unsigned vpr = static_cast<unsigned>(L.head_dim) / 8u;
+  const unsigned per_plane = static_cast<unsigned>(chunk_len) * vpr;
+  const unsigned page_vecs = static_cast<unsigned>(L.page_tokens) * vpr;
+  const unsigned long long planes_per_page = static_cast<unsigned long long>(L.n_layers) * 2u * L.n_kv_heads;
+  const unsigned plane = v / per_plane;
+  const unsigned rem = v - plane * per_plane;
+  const unsigned t = rem / vpr;
+  const unsigned d = rem - t * vpr;
+  const unsigned pg = t / static_cast<unsigned>(L.page_tokens);
+  const unsigned slot = t - pg * static_cast<unsigned>(L.page_tokens);
+  const unsigned long long phys = static_cast<unsigned long long>(block_table[first_page + pg]);
+  return (phys * planes_per_page + plane) * page_vecs + slot * vpr + d;
+}
+
+__device__ __forceinline__ float q8_level_value(float lo, float span, unsigned q) {
+  return span <= 0.0f ? lo : __fadd_rn(lo, __fmul_rn(__fdiv_rn(static_cast<float>(q), 255.0f), span));
+}
+
+// One thread per 16 encoded bytes -> 16 bf16 = two pool vectors of the same
+// token row (head_dim/8 is even). payload: 16-B aligned (header just before).
+__global__ void kv_scatter_q8_kernel(const uint4* __restrict__ payload, const __half* __restrict__ hdr,
+                                     uint4* __restrict__ pool, const int* __restrict__ block_table,
+                                     long long first_page, int chunk_len, KvLayout L, unsigned n16) {
+  const float lo = __half2float(hdr[0]);
+  const float span = __half2float(hdr[1]) - lo;
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < n16; v += gridDim.x * blockDim.x) {
+    const uint4 q = payload[v];
+    const unsigned w[4] = {q.x, q.y, q.z, q.w};
+    uint32_t o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const unsigned b0 = (w[i >> 1] >> ((i & 1) * 16)) & 0xFFu;
+      const unsigned b1 = (w[i >> 1] >> ((i & 1) * 16 + 8)) & 0xFFu;
+      const __nv_bfloat162 h2 = __floats2bfloat162_rn(q8_level_value(lo, span, b0), q8_level_value(lo, span, b1));
+      o[i] = *reinterpret_cast<const uint32_t*>(&h2);
+    }
+    const unsigned long long dst = kv_pool_vec(2u * v, block_table, first_page, chunk_len, L);
+    pool[dst] = make_uint4(o[0], o[1], o[2], o[3]);
+    pool[dst + 1] = make_uint4(o[4], o[5], o[6], o[7]);
+  }
+}
+
+__device__ __forceinline__ unsigned float_order_key(float f) {
+  const unsigned b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float float_from_order_key(unsigned k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
+// ws[0] = ordered-min key, ws[1] = ordered-max key (caller: 0xFFFFFFFF / 0).
+__global__ void kv_minmax_kernel(const uint4* __restrict__ x, unsigned n8, unsigned* __restrict__ ws) {
+  unsigned kmin = 0xFFFFFFFFu, kmax = 0u;
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < n8; v += gridDim.x * blockDim.x) {
+    const uint4 q = x[v];
+    const unsigned w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+      kmin = min(kmin, min(float_order_key(f.x), float_order_key(f.y)));
+      kmax = max(kmax, max(float_order_key(f.x), float_order_key(f.y)));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&ws[0], kmin);
+    atomicMax(&ws[1], kmax);
+  }
+}
+
+// 8 bf16 -> 8 levels per thread; out = header (4 B) + payload, 4-B aligned.
+__global__ void kv_quant8_kernel(const uint4* __restrict__ x, unsigned n8, const unsigned* __restrict__ ws,
+                                 uint8_t* __restrict__ out) {
+  const float lo = float_from_order_key(ws[0]);
+  const float hi = float_from_order_key(ws[1]);
+  const float span = hi - lo;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __half* h = reinterpret_cast<__half*>(out);
+    h[0] = __float2half_rn(lo);
+    h[1] = __float2half_rn(hi);
+  }
+  uint32_t* q = reinterpret_cast<uint32_t*>(out + 4);
+  for (unsigned v = blockIdx.x * blockDim.x + threadIdx.x; v < n8; v += gridDim.x * blockDim.x) {
+    const uint4 in = x[v];
+    const unsigned w[4] = {in.x, in.y, in.z, in.w};
+    unsigned lv[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+      const float e[2] = {f.x, f.y};
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        float l = 0.0f;
+        if (span > 0.0f) l = roundf(__fmul_rn(__fdiv_rn(__fsub_rn(e[j], lo), span), 255.0f));
+        lv[2 * i + j] = static_cast<unsigned>(fminf(fmaxf(l, 0.0f), 255.0f));
+      }
+    }
+    q[2 * v] = lv[0] | (lv[1] << 8) | (lv[2] << 16) | (lv[3] << 24);
+    q[2 * v + 1] = lv[4] | (lv[5] << 8) | (lv[6] << 16) | (lv[7] << 24);
+  }
+}
+
 }  // namespace cake_dev

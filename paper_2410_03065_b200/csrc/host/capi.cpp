@@ -134,6 +134,7 @@ struct cake_store {
 #ifndef CAKE_REFERENCE_BUILD
 struct cake_gpu {
   std::unique_ptr<GpuContext> ctx;
+  Codec codec = Codec::identity();  // cache-tier codec of build_tier and run
 };
 #endif
 
@@ -399,7 +400,15 @@ int cake_gpu_build_tier(cake_gpu* g, cake_store* s, uint64_t total_tokens, uint3
     RequestSpec req;
     req.total_tokens = total_tokens;
     req.chunk_size = chunk_size;
-    g->ctx->build_cache_tier(s->store, req, prompt_seed);
+    g->ctx->build_cache_tier(s->store, req, prompt_seed, g->codec);
+  });
+}
+
+int cake_gpu_set_codec(cake_gpu* g, const char* codec_id) {
+  return guarded([&] {
+    const Codec c = Codec::parse(codec_id ? codec_id : "identity");
+    if (c.kind == Codec::Kind::factor) throw std::invalid_argument("gpu: the factor codec models bytes only");
+    g->codec = c;
   });
 }
 
@@ -425,7 +434,7 @@ int cake_gpu_run(cake_gpu* g, cake_store* s, uint64_t total_tokens, uint32_t chu
     o.gpu = g->ctx.get();
     const GpuModelConfig& mc = g->ctx->config();
     const ModelProfile prof = mc.profile(g->ctx->options().tp_size);
-    const RunReport r = run(req, prof, g->ctx->options().prior, to_trace(trace), Codec::identity(), to_mode(mode),
+    const RunReport r = run(req, prof, g->ctx->options().prior, to_trace(trace), g->codec, to_mode(mode),
                             ClockMode::live, s->store, prompt_seed, o);
     const GpuRunInfo& info = g->ctx->last_run();
     if (res) {

@@ -237,7 +237,8 @@ void upload_tokens(GpuContext::Impl& g, const std::vector<std::uint32_t>& ids, v
 
 }  // namespace
 
-PopulateResult GpuContext::build_cache_tier(ChunkStore& store, const RequestSpec& request, std::uint64_t prompt_seed) {
+PopulateResult GpuContext::build_cache_tier(ChunkStore& store, const RequestSpec& request, std::uint64_t prompt_seed,
+                                            const Codec& codec) {
   Impl& g = *impl_;
   request.validate();
   const auto chunks = split_into_chunks(request.total_tokens, request.chunk_size);
@@ -245,6 +246,8 @@ PopulateResult GpuContext::build_cache_tier(ChunkStore& store, const RequestSpec
   const auto ids = token_stream(prompt_seed, request.total_tokens);
   upload_tokens(g, ids, g.s_compute);
   check(cake_memset_async(g.abort_flags.p, 0, g.n_pages * sizeof(std::int32_t), g.s_compute), "memset");
+  if (codec.kind == Codec::Kind::factor) throw std::invalid_argument("gpu tier: the factor codec models bytes only");
+  const bool q8 = codec.kind == Codec::Kind::quant8;
   const ModelProfile prof = g.cfg.profile(g.opt.tp_size);
   Pinned<std::byte> host;
   host.reset(g.staging_bytes);
@@ -258,20 +261,29 @@ PopulateResult GpuContext::build_cache_tier(ChunkStore& store, const RequestSpec
     check(cake_kv_gather(g.model, g.staging[0].p, static_cast<long long>(c.token_start), static_cast<int>(c.token_count),
                          g.bt_primary.p, g.s_compute),
           "gather");
-    check(cake_d2h_async(host.p, g.staging[0].p, bytes, g.s_compute), "D2H");
+    std::size_t enc = bytes;
+    if (q8) {
+      enc = static_cast<std::size_t>(cake_kv_q8_bytes(g.model, static_cast<int>(c.token_count)));
+      check(cake_kv_encode_q8(g.model, g.staging[0].p, static_cast<int>(c.token_count), g.staging[1].p, g.s_compute),
+            "q8 encode");
+      check(cake_d2h_async(host.p, g.staging[1].p, enc, g.s_compute), "D2H");
+    } else {
+      check(cake_d2h_async(host.p, g.staging[0].p, bytes, g.s_compute), "D2H");
+    }
     check(cake_stream_sync(g.s_compute), "sync");
     const ChunkKey key =
         chain_hash(prev, std::span<const std::uint32_t>(ids.data() + c.token_start, c.token_count));
     prev = key;
     res.keys.push_back(key);
     if (bytes != chunk_bytes(prof, c)) throw std::logic_error("gpu: chunk bytes disagree with the KV profile");
-    const ChunkMeta meta{c.token_count, "identity", bytes, bytes};
+    if (enc != codec.encoded_size(bytes)) throw std::logic_error("gpu: encoded size disagrees with the codec law");
+    const ChunkMeta meta{c.token_count, codec.id(), enc, bytes};
     if (store.contains(key)) {
       ++res.chunks_existing;
       continue;
     }
-    store.put(key, std::span<const std::byte>(host.p, bytes), meta);
-    res.bytes_written += bytes;
+    store.put(key, std::span<const std::byte>(host.p, enc), meta);
+    res.bytes_written += enc;
     ++res.chunks_written;
   }
   return res;
@@ -505,13 +517,14 @@ class GpuPrefillBackend final : public PrefillBackend {
 
 class GpuLoaderSink final : public ChunkSink {
  public:
-  explicit GpuLoaderSink(LiveRun& run) : r_(run) {}
+  GpuLoaderSink(LiveRun& run, bool q8) : r_(run), q8_(q8) {}
 
   void begin_chunk(const FetchTask& t) override {
     GpuContext::Impl& g = r_.g;
     if (r_.tp) r_.tp->publish_io(t.chunk.index);  // every rank loads its shard of this chunk
     if (t.contested) r_.start_race(t.chunk, kByIo, g.s_copy);
-    buf_ = g.staging[parity_].p;
+    // quant8: land the 4-B header at +12 so the level payload is 16-B aligned
+    buf_ = g.staging[parity_].p + (q8_ ? kQ8Offset : 0);
     parity_ ^= 1;
   }
 
@@ -522,9 +535,15 @@ class GpuLoaderSink final : public ChunkSink {
 
   void end_chunk(const FetchTask& t) override {
     GpuContext::Impl& g = r_.g;
-    check(cake_kv_scatter(g.model, buf_, static_cast<long long>(t.chunk.token_start), static_cast<int>(t.chunk.token_count),
-                          r_.table_for(t.chunk.index, kByIo), 0, static_cast<long long>(t.encoded_bytes), g.s_copy),
-          "scatter");
+    if (q8_)
+      check(cake_kv_scatter_q8(g.model, buf_, static_cast<long long>(t.chunk.token_start),
+                               static_cast<int>(t.chunk.token_count), r_.table_for(t.chunk.index, kByIo), g.s_copy),
+            "q8 decode-scatter");
+    else
+      check(cake_kv_scatter(g.model, buf_, static_cast<long long>(t.chunk.token_start),
+                            static_cast<int>(t.chunk.token_count), r_.table_for(t.chunk.index, kByIo), 0,
+                            static_cast<long long>(t.encoded_bytes), g.s_copy),
+            "scatter");
     check(cake_event_record(g.ev_io[t.chunk.index]->h, g.s_copy), "record");
   }
 
@@ -546,7 +565,9 @@ class GpuLoaderSink final : public ChunkSink {
   std::uint64_t h2d_bytes() const { return h2d_bytes_; }
 
  private:
+  static constexpr std::size_t kQ8Offset = 12;
   LiveRun& r_;
+  bool q8_;
   std::byte* buf_ = nullptr;
   int parity_ = 0;
   std::uint64_t h2d_bytes_ = 0;
@@ -597,7 +618,8 @@ RunReport run_follower(GpuContext::Impl& g, TpCoordinator& tp, const RunPlan& pl
           if (rd.read(host) != host.size()) throw CorruptChunkError("tp follower: short read");
           src = host.data();
         }
-        std::byte* buf = g.staging[k & 1].p;
+        const bool q8 = plan.encoded_bytes[i] != plan.uncompressed_bytes[i];
+        std::byte* buf = g.staging[k & 1].p + (q8 ? 12 : 0);
         for (std::uint64_t off = 0; off < total;) {
           const std::uint64_t len = std::min(quantum, total - off);
           const Micros gate = budget + time_to_transfer_bits(trace, len * 8, budget);
@@ -609,10 +631,15 @@ RunReport run_follower(GpuContext::Impl& g, TpCoordinator& tp, const RunPlan& pl
           const Micros one = time_to_transfer_bits(trace, quantum * 8, budget);
           if (budget + one < now) budget = now - one;
         }
-        check(cake_kv_scatter(g.model, buf, static_cast<long long>(plan.chunks[i].token_start),
-                              static_cast<int>(plan.chunks[i].token_count), g.bt_primary.p, 0,
-                              static_cast<long long>(total), g.s_copy),
-              "scatter");
+        if (q8)
+          check(cake_kv_scatter_q8(g.model, buf, static_cast<long long>(plan.chunks[i].token_start),
+                                   static_cast<int>(plan.chunks[i].token_count), g.bt_primary.p, g.s_copy),
+                "q8 decode-scatter");
+        else
+          check(cake_kv_scatter(g.model, buf, static_cast<long long>(plan.chunks[i].token_start),
+                                static_cast<int>(plan.chunks[i].token_count), g.bt_primary.p, 0,
+                                static_cast<long long>(total), g.s_copy),
+                "scatter");
         check(cake_event_record(g.ev_io[i]->h, g.s_copy), "record");
         check(cake_event_sync(g.ev_io[i]->h), "io wait");
         tp.shard_landed(i);
@@ -664,7 +691,7 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
                        const BandwidthTrace& trace, const Codec& codec, const ChunkStore& store, RunMode mode,
                        double power, const RunOptions& opt) {
   GpuContext::Impl& g = *opt.gpu->impl();
-  if (codec.kind != Codec::Kind::identity) throw std::invalid_argument("gpu run: only the identity codec is wired");
+  if (codec.kind == Codec::Kind::factor) throw std::invalid_argument("gpu run: the factor codec models bytes only");
   const auto n = static_cast<std::uint32_t>(plan.chunks.size());
   check_chunking(g, plan.chunks, tokens.size());
   for (std::uint32_t i = 0; i < n; ++i)
@@ -695,7 +722,7 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   info.h2d_bytes = tokens.size() * sizeof(std::int32_t);
 
   ClaimTable table(n);
-  GpuLoaderSink sink(run);
+  GpuLoaderSink sink(run, codec.kind == Codec::Kind::quant8);
   GpuPrefillBackend backend(run, opt.gpu->options().prior);
   std::unique_ptr<TransferEngine> loader;
   if (io_on) {

@@ -96,6 +96,7 @@ _SIGS = {
     "cake_gpu_destroy": (C.c_int, [vp]),
     "cake_gpu_kv_bytes_per_token": (C.c_int, [vp, P(u64)]),
     "cake_gpu_build_tier": (C.c_int, [vp, vp, u64, u32, u64]),
+    "cake_gpu_set_codec": (C.c_int, [vp, C.c_char_p]),
     "cake_gpu_calibrate": (C.c_int, [vp, u64, u32, u64, P(dbl), P(dbl)]),
     "cake_gpu_run": (C.c_int, [vp, vp, u64, u32, u64, CakeTrace, C.c_int, P(CakeRunOpts), P(CakeGpuResult),
                                P(CakeRecord)]),
@@ -199,6 +200,10 @@ def load_cuda():
     lib.cake_kv_chunk_bytes.argtypes = [vp, C.c_int]
     lib.cake_kv_scatter.argtypes = [vp, vp, C.c_longlong, C.c_int, vp, C.c_longlong, C.c_longlong, vp]
     lib.cake_kv_gather.argtypes = [vp, vp, C.c_longlong, C.c_int, vp, vp]
+    lib.cake_kv_q8_bytes.restype = C.c_longlong
+    lib.cake_kv_q8_bytes.argtypes = [vp, C.c_int]
+    lib.cake_kv_scatter_q8.argtypes = [vp, vp, C.c_longlong, C.c_int, vp, vp]
+    lib.cake_kv_encode_q8.argtypes = [vp, vp, C.c_int, vp, vp]
     lib.cake_prefill_group.argtypes = [C.POINTER(vp), C.c_int, vp, C.c_longlong, C.c_int, vp, vp]
     lib.cake_final_logits.argtypes = [vp, C.c_longlong, vp, C.c_int, C.c_int, vp, vp, vp]
     lib.cake_nccl_unique_id.argtypes = [vp]

@@ -93,6 +93,12 @@ class GpuRuntime:
         self.n.call("cake_gpu_build_tier", self.h, store.h, total_tokens, chunk_size, prompt_seed)
         return store
 
+    def set_codec(self, codec: str = "identity"):
+        """Cache-tier codec for build_cache_tier and run: "identity" | "quant8"
+        (reference codec.cpp:114-162; the GPU decodes inside the scatter)."""
+        self.n.call("cake_gpu_set_codec", self.h, codec.encode())
+        self.codec = codec
+
     def calibrate(self, total_tokens: int, chunk_size: int, prompt_seed: int):
         a, b = N.dbl(), N.dbl()
         self.n.call("cake_gpu_calibrate", self.h, total_tokens, chunk_size, prompt_seed, C.byref(a), C.byref(b))
