@@ -67,6 +67,23 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (degree-3 minimax of 2^f on [-0.5, 0.5], rel err 7.5e-5,
+// well under bf16's 2^-8): a share of the softmax exponentials is computed here
+// so the MUFU unit (16/clk/SM, the softmax bottleneck) is not the critical
+// pipe next to the tensor core. x <= ~8 here; clamped below at -125 so the
+// exponent add cannot wrap (2^-125 is 0 for the bf16 P and the fp32 sum).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.0f);
+  const float t = __fadd_rn(x, 12582912.0f);  // 1.5 * 2^23: round(x) lands in the low mantissa bits
+  const float f = __fsub_rn(x, __fsub_rn(t, 12582912.0f));
+  float p = fmaf(0.05517132f, f, 0.24261054f);
+  p = fmaf(p, f, 0.69326099f);
+  p = fmaf(p, f, 0.99992811f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+// pairs i of the 32 per half-block row whose exponentials go to ex2_poly
+constexpr unsigned kFaPolyPairs = 0x88888888u;  // every 4th pair: 25%
+
 template <int HD>
 __global__ void __launch_bounds__(kFaThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
@@ -324,8 +341,10 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       uint32_t pk[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
-        const float p0 = ex2_approx(fmaf(sv[2 * i], sc, nbase));
-        const float p1 = ex2_approx(fmaf(sv[2 * i + 1], sc, nbase));
+        const bool poly = (kFaPolyPairs >> i) & 1u;
+        const float x0 = fmaf(sv[2 * i], sc, nbase), x1 = fmaf(sv[2 * i + 1], sc, nbase);
+        const float p0 = poly ? ex2_poly(x0) : ex2_approx(x0);
+        const float p1 = poly ? ex2_poly(x1) : ex2_approx(x1);
         rs0 += p0;
         rs1 += p1;
         pk[i] = pack_bf16(p0, p1);
