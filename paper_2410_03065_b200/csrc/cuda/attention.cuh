@@ -311,6 +311,8 @@ template <int HD>
 __global__ void attn_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_lse,
                                     __nv_bfloat16* __restrict__ out, int rows, int num_splits,
                                     const int* abort_flag) {
+  pdl_wait();
+  pdl_trigger();
   if (abort_flag != nullptr && *(volatile const int*)abort_flag) return;
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;

@@ -91,9 +91,6 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   using Cfg = FaCfg<HD>;
   extern __shared__ uint8_t smem_raw[];
   __shared__ int s_abort;
-  if (threadIdx.x == 0) s_abort = a.abort_flag != nullptr ? *(volatile const int*)a.abort_flag : 0;
-  __syncthreads();
-  if (s_abort) return;
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = lane_id();
@@ -102,7 +99,6 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   const int G = a.n_q_heads / a.n_kv_heads;
   const int tok_per_tile = kFaRows / G;
   const int tok0 = blockIdx.x * tok_per_tile;
-  if (tok0 >= a.chunk_len) return;
   const int tok_last = min(tok0 + tok_per_tile, a.chunk_len) - 1;
   const long long kv_end = a.chunk_start + tok_last + 1;
   const int n_pages = static_cast<int>((kv_end + kAttnPage - 1) / kAttnPage);
@@ -148,10 +144,18 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  // (PDL) everything above overlaps the predecessor's tail; Q / the KV pool are read below
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) s_abort = a.abort_flag != nullptr ? *(volatile const int*)a.abort_flag : 0;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (s_abort || tok0 >= a.chunk_len) {
+    if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tmem);
+    return;
+  }
 
   const long long planes = static_cast<long long>(a.n_layers) * 2 * a.n_kv_heads;
   auto page_row = [&](int lp, int kv) -> int32_t {  // first pool row of (page, layer, K|V, kv head)

@@ -65,6 +65,46 @@ int fail(int code, const char* fmt, ...) {
 
 cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Programmatic dependent launch for the chunk's kernel chain (every kernel
+// launched here calls pdl_wait() before touching its predecessor's outputs):
+// the next kernel's CTAs become resident and run their prologue (barrier
+// init, TMEM alloc, descriptor prefetch) while the previous kernel drains.
+// CAKE_PDL=0 turns it off (A/B measurements).
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CAKE_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
+                         Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (cluster > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ------------------------------------------------------------ TMA maps
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -198,9 +238,8 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaSt
   // stream-K: every cluster gets >= 8 k-blocks (>= 1 unit, so none is empty); all clusters co-resident
   const long long work = a.whole_tiles ? static_cast<long long>(m_groups) * a.num_n_blocks : units / 8;
   const int clusters = static_cast<int>(std::max<long long>(1, std::min<long long>(max_clusters[ci], work)));
-  cfg.gridDim = dim3(clusters * a.cs);
   CKS(streamk_scratch(&a.sk_ws, &a.sk_flags, &a.epoch));
-  CK(cudaLaunchKernelEx(&cfg, kern, ta, tb, a));
+  CK(launch_chain(kern, dim3(clusters * a.cs), dim3(kGemmThreads), Cfg::kSmemBytes, s, a.cs, ta, tb, a));
   return CAKE_OK;
 }
 
@@ -258,9 +297,8 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
     a.whole_tiles = split == 1 ? 1 : 0;
     pairs = split == 1 ? std::min(tiles, max_pairs) : tiles * split;
   }
-  cfg.gridDim = dim3(2 * pairs);
   CKS(streamk_scratch(&a.sk_ws, &a.sk_flags, &a.epoch));
-  CK(cudaLaunchKernelEx(&cfg, kern, ta, tb_half, a));
+  CK(launch_chain(kern, dim3(2 * pairs), dim3(kGemmThreads), Cfg::kSmemBytes, s, 2, ta, tb_half, a));
   return CAKE_OK;
 }
 
@@ -506,14 +544,14 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
         CK(cudaFuncSetAttribute(attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, FaCfg<128>::kSmem));
         cfgd = true;
       }
-      attn_tc_kernel<128><<<grid, kFaThreads, FaCfg<128>::kSmem, s>>>(m->tm_q, m->tm_kv, fa);
+      CK(launch_chain(attn_tc_kernel<128>, grid, dim3(kFaThreads), FaCfg<128>::kSmem, s, 1, m->tm_q, m->tm_kv, fa));
     } else {
       static bool cfgd = false;
       if (!cfgd) {
         CK(cudaFuncSetAttribute(attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, FaCfg<64>::kSmem));
         cfgd = true;
       }
-      attn_tc_kernel<64><<<grid, kFaThreads, FaCfg<64>::kSmem, s>>>(m->tm_q, m->tm_kv, fa);
+      CK(launch_chain(attn_tc_kernel<64>, grid, dim3(kFaThreads), FaCfg<64>::kSmem, s, 1, m->tm_q, m->tm_kv, fa));
     }
     CKL();
   } else {
@@ -555,11 +593,13 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
     const int rows = chunk_len * m->nq;
     const int wpb = 8;
     if (m->hd == 128)
-      attn_combine_kernel<128><<<(rows + wpb - 1) / wpb, wpb * 32, 0, s>>>(m->part_o, m->part_lse, m->attn, rows, splits,
-                                                                          abort_flag);
+      CK(launch_chain(attn_combine_kernel<128>, dim3((rows + wpb - 1) / wpb), dim3(wpb * 32), 0, s, 1,
+                      static_cast<const float*>(m->part_o), static_cast<const float*>(m->part_lse), m->attn, rows,
+                      splits, abort_flag));
     else
-      attn_combine_kernel<64><<<(rows + wpb - 1) / wpb, wpb * 32, 0, s>>>(m->part_o, m->part_lse, m->attn, rows, splits,
-                                                                         abort_flag);
+      CK(launch_chain(attn_combine_kernel<64>, dim3((rows + wpb - 1) / wpb), dim3(wpb * 32), 0, s, 1,
+                      static_cast<const float*>(m->part_o), static_cast<const float*>(m->part_lse), m->attn, rows,
+                      splits, abort_flag));
     CKL();
   }
   return CAKE_OK;
@@ -576,7 +616,7 @@ int launch_skinny(cake_model* m, int kind, const SkinnyArgs& a, double rows, cud
   const int smem = a.M * a.K * 2;
   const int blocks = std::max(1, std::min((a.units + kSkinnyWarps - 1) / kSkinnyWarps, num_sms() * 16));
   ProfScope ps(m, kind, s, 2.0 * a.M * rows * a.K, 2.0 * rows * a.K);
-  kern<<<blocks, kSkinnyWarps * 32, smem, s>>>(a);
+  CK(launch_chain(kern, dim3(blocks), dim3(kSkinnyWarps * 32), smem, s, 1, a));
   CKL();
   return CAKE_OK;
 }
@@ -657,8 +697,9 @@ int last_token_pass(cake_model* m, const int32_t* d_token, long long T, const in
 
 int rmsnorm(cake_model* m, const bf16* gamma, long long row0, int rows, const int32_t* abort_flag, cudaStream_t s) {
   ProfScope ps(m, CAKE_K_RMSNORM, s, 0.0, static_cast<double>(rows) * m->H * 6);
-  rmsnorm_kernel<<<(rows + kNormRowsPerCta - 1) / kNormRowsPerCta, kNormThreadsPerRow * kNormRowsPerCta, 0, s>>>(
-      m->h, gamma, m->xn, m->H, m->cfg.rms_eps, row0, rows, abort_flag);
+  CK(launch_chain(rmsnorm_kernel, dim3((rows + kNormRowsPerCta - 1) / kNormRowsPerCta),
+                  dim3(kNormThreadsPerRow * kNormRowsPerCta), 0, s, 1, static_cast<const float*>(m->h), gamma, m->xn,
+                  m->H, m->cfg.rms_eps, row0, rows, abort_flag));
   CKL();
   return CAKE_OK;
 }
@@ -1168,7 +1209,8 @@ int cake_prefill_layers(cake_model* m, const int32_t* d_tokens, long long chunk_
   const int H = m->H;
   if (layer_begin == 0) {
     ProfScope ps(m, CAKE_K_EMBED, s, 0.0, static_cast<double>(M) * H * 6);
-    embed_kernel<<<M, 128, 0, s>>>(d_tokens, m->embed, m->h, H, d_abort);
+    CK(launch_chain(embed_kernel, dim3(M), dim3(128), 0, s, 1, d_tokens, static_cast<const bf16*>(m->embed), m->h, H,
+                    d_abort));
     CKL();
   }
   const bool no_kv = (flags & CAKE_PREFILL_NO_KV_WRITE) != 0;

@@ -64,6 +64,8 @@ __global__ void fill_bf16_kernel(__nv_bfloat16* dst, long long n, float v) {
 // h[m, :] = embed[token[m], :] (fp32 residual stream). One CTA per token.
 __global__ void embed_kernel(const int* __restrict__ tokens, const __nv_bfloat16* __restrict__ table,
                              float* __restrict__ h, int hidden, const int* abort_flag) {
+  pdl_wait();
+  pdl_trigger();
   if (abort_flag != nullptr && *(volatile const int*)abort_flag) return;
   const int m = blockIdx.x;
   const __nv_bfloat16* row = table + static_cast<size_t>(tokens[m]) * hidden;
@@ -95,6 +97,8 @@ __global__ void __launch_bounds__(kNormThreadsPerRow* kNormRowsPerCta)
     rmsnorm_kernel(const float* __restrict__ h, const __nv_bfloat16* __restrict__ gamma,
                    __nv_bfloat16* __restrict__ y, int hidden, float eps, long long row0, int rows,
                    const int* abort_flag) {
+  pdl_wait();
+  pdl_trigger();
   if (abort_flag != nullptr && *(volatile const int*)abort_flag) return;
   __shared__ float red[kNormRowsPerCta][kNormThreadsPerRow / 32];
   const int sub = threadIdx.x / kNormThreadsPerRow;
@@ -140,6 +144,8 @@ __global__ void __launch_bounds__(kNormThreadsPerRow* kNormRowsPerCta)
 // h += p (tensor-parallel: residual += all-reduced partial sums)
 __global__ void add_inplace_kernel(float* __restrict__ h, const float* __restrict__ p, long long n,
                                    const int* abort_flag) {
+  pdl_wait();
+  pdl_trigger();
   if (abort_flag != nullptr && *(volatile const int*)abort_flag) return;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n / 4;
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -158,6 +164,8 @@ __global__ void add_inplace_kernel(float* __restrict__ h, const float* __restric
 // in shared memory as fp32. Memory-bound: reads W exactly once.
 __global__ void gemv_kernel(const __nv_bfloat16* __restrict__ W, const __nv_bfloat16* __restrict__ x,
                             float* __restrict__ y, int N, int K) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float xs[];
   for (int i = threadIdx.x; i < K; i += blockDim.x) xs[i] = __bfloat162float(x[i]);
   __syncthreads();

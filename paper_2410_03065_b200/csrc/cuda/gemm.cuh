@@ -302,10 +302,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   extern __shared__ uint8_t smem_raw[];
 
   __shared__ int s_abort;
-  if (threadIdx.x == 0) s_abort = (args.abort_flag != nullptr) ? *(volatile const int*)args.abort_flag : 0;
-  __syncthreads();
-  if (s_abort) return;
-
   const uint32_t raw_base = smem_u32(smem_raw);
   const uint32_t pad = ((raw_base + 1023u) & ~1023u) - raw_base;
   uint8_t* smem = smem_raw + pad;
@@ -334,10 +330,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  // (PDL) everything above overlaps the predecessor's tail; its outputs are read below
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) s_abort = (args.abort_flag != nullptr) ? *(volatile const int*)args.abort_flag : 0;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (args.cs > 1) {
+    // one abort decision per cluster (rank 0's): a lone CTA leaving would strand its peers' multicasts
+    cluster_sync();
+    const int ab = ld_shared_cluster_s32(mapa_shared(smem_u32(&s_abort), 0));
+    __syncthreads();
+    if (ab) {
+      cluster_sync();
+      if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+      return;
+    }
+  } else if (s_abort) {
+    if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    return;
+  }
 
   const int nk = args.num_k_blocks;
   const int cs = args.cs;
@@ -349,7 +363,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int m_groups = (args.num_m_blocks + cs - 1) / cs;
   const long long units = static_cast<long long>(m_groups) * args.num_n_blocks * nk;
   int tile, kb0, kb1;
-  if (cs > 1) cluster_sync();  // peers' barriers are initialised before any multicast
 
   if (warp == 0) {
     if (lane == 0) {

@@ -46,15 +46,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
-  // One abort decision per pair (a lone CTA leaving would strand its peer).
-  if (threadIdx.x == 0) s_abort = (args.abort_flag != nullptr) ? *(volatile const int*)args.abort_flag : 0;
-  cluster_sync();
-  const int abort_pair = ld_shared_cluster_s32(mapa_shared(smem_u32(&s_abort), 0));
-  if (abort_pair) {
-    cluster_sync();
-    return;
-  }
-
   const uint32_t raw_base = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_base + 1023u) & ~1023u) - raw_base);
   uint8_t* smem_a = smem;
@@ -81,10 +72,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc_2sm<Cfg::kTmemCols>(tmem_slot);
+  // (PDL) everything above overlaps the predecessor's tail; its outputs are read below
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) s_abort = (args.abort_flag != nullptr) ? *(volatile const int*)args.abort_flag : 0;
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // One abort decision per pair, the leader's (a lone CTA leaving would strand its peer).
+  const int abort_pair = ld_shared_cluster_s32(mapa_shared(smem_u32(&s_abort), 0));
+  if (abort_pair) {
+    cluster_sync();
+    if (warp == 1) tmem_dealloc_2sm<Cfg::kTmemCols>(tmem_base);
+    return;
+  }
 
   const int pair = blockIdx.x / 2;
   const int n_pairs = gridDim.x / 2;

@@ -33,6 +33,19 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may become resident while
+// its predecessor on the stream is still draining. Everything before
+// pdl_wait() (barrier init, TMEM alloc, descriptor prefetch) must not touch
+// global memory the predecessor writes or reads; pdl_wait() returns once the
+// predecessor grid has completed and its writes are visible. Every CTA calls
+// pdl_wait() before it exits (an early-exiting grid would otherwise "complete"
+// ahead of its predecessor and release its own successor too early). Without
+// the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

@@ -76,6 +76,8 @@ __device__ __forceinline__ void skinny_dot(const __nv_bfloat16* const (&w)[NR], 
 
 template <int EPI>
 __global__ void __launch_bounds__(kSkinnyWarps * 32) skinny_kernel(const SkinnyArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) uint8_t sm[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm);
   const int total = a.M * a.K;

@@ -694,9 +694,11 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   if (codec.kind == Codec::Kind::factor) throw std::invalid_argument("gpu run: the factor codec models bytes only");
   const auto n = static_cast<std::uint32_t>(plan.chunks.size());
   check_chunking(g, plan.chunks, tokens.size());
-  for (std::uint32_t i = 0; i < n; ++i)
-    if (plan.encoded_bytes[i] != static_cast<std::uint64_t>(cake_kv_chunk_bytes(g.model, plan.chunks[i].token_count)))
+  for (std::uint32_t i = 0; i < n; ++i) {
+    const auto raw = static_cast<std::uint64_t>(cake_kv_chunk_bytes(g.model, plan.chunks[i].token_count));
+    if (plan.encoded_bytes[i] != codec.encoded_size(raw))
       throw std::invalid_argument("gpu run: cache-tier chunk size disagrees with the model's KV layout");
+  }
   const bool io_on = mode == RunMode::io_only || (mode == RunMode::cake && opt.io_enabled);
   const bool compute_on = mode == RunMode::compute_only || (mode == RunMode::cake && opt.compute_enabled);
   if (!io_on && !compute_on) throw std::invalid_argument("run: no side enabled");

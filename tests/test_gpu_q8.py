@@ -54,7 +54,8 @@ def test_gpu_decode_scatter_matches_oracle(q8setup):
 
     rt, tier_id, tier_q8, keys = q8setup
     r = rt.run(tier_q8, T, C, SEED, mbps=8000, mode="io_only")
-    assert r.h2d_bytes == sum(len(tier_q8.get(k)) for k in keys)
+    # every loaded byte is the quant8 payload; the only other upload is the prompt's token ids
+    assert r.h2d_bytes == sum(len(tier_q8.get(k)) for k in keys) + 4 * T
     for i, k in enumerate(keys):
         raw_len = len(tier_id.get(k))
         want = kvcodec.q8_decode(tier_q8.get(k), raw_len, "bf16")
