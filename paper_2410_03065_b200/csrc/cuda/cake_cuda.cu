@@ -173,6 +173,8 @@ struct StreamKScratch {
 StreamKScratch g_sk;
 int g_gemm_schedule = 0;  // 0 whole tiles (+ exact split-K when tiles < SM pairs), 1 stream-K
 int g_gemm_2sm = 1;       // 1: M > 128 projections use the 2-SM (cta_group::2) kernel
+int g_gemm_2sm_n128 = 0;  // experiment: O / down (N tiles of 128) on CTA pairs too
+int g_gemm_hints = 3;     // L2 policy of the operand loads (GemmArgs::l2_hints)
 
 int streamk_scratch(float** ws, int** flags, int* epoch) {
   std::lock_guard<std::mutex> lk(g_sk.mu);
@@ -246,10 +248,10 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaSt
 // 2-SM GEMM: pairs of CTAs on 256 x 256 tiles. Few tiles (O / down at M = 512:
 // 32) are split along K into S equal parts so the pairs fill the GPU; the
 // k = 0 part owns the tile and adds the others (deterministic order).
-template <int EPI>
+template <int BLOCK_N, int EPI>
 int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, cudaStream_t s) {
-  using Cfg = Gemm2Cfg;
-  auto kern = gemm2_tc_kernel<EPI>;
+  using Cfg = Gemm2Cfg<BLOCK_N>;
+  auto kern = gemm2_tc_kernel<BLOCK_N, EPI>;
   static bool configured = false;
   static int max_pairs = 0;
   cudaLaunchConfig_t cfg{};
@@ -276,7 +278,7 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
     configured = true;
   }
   a.num_m_blocks = (a.M + kGemmBlockM - 1) / kGemmBlockM;
-  a.num_n_blocks = a.N / kGemm2BlockN;
+  a.num_n_blocks = a.N / BLOCK_N;
   a.num_k_blocks = a.K / kGemmBlockK;
   a.cs = 2;
   const int m_pairs = (a.num_m_blocks + 1) / 2;
@@ -289,7 +291,8 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
   } else {
     // split parts run concurrently (the owner waits for its partner): keep
     // tiles * split within the SM pairs so every part is resident together
-    const int pair_budget = num_sms() / 2;
+    static const bool no_split = std::getenv("CAKE_GEMM_NOSPLIT") != nullptr;  // experiments: one pair per tile
+    const int pair_budget = no_split ? 0 : num_sms() / 2;
     int split = 1;
     while (tiles * (split + 1) <= pair_budget && a.num_k_blocks % (split + 1) == 0 &&
            a.num_k_blocks / (split + 1) >= 8)
@@ -302,22 +305,43 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
   return CAKE_OK;
 }
 
-int gemm_dispatch(int bn, int epi, const CUtensorMap& ta, const CUtensorMap* tb3, const GemmArgs& a,
+int gemm_dispatch(int bn, int epi, const CUtensorMap& ta, const CUtensorMap* tb3, const GemmArgs& a_in,
                   cudaStream_t s) {
-  // 2-SM tiles pay off when they alone fill most SM pairs (QKV: 48, gate/up: 224 at
-  // M = 512); few-tile projections (O, down: 32) stay on 1-SM 128 x 128 tiles,
-  // measured faster than 2-SM + split-K (tools/gemm_fixed_cost.py).
-  const int pair_tiles = ((a.M + 255) / 256) * (a.N / kGemm2BlockN);
-  if (g_gemm_2sm && a.M > kGemmBlockM && a.N % kGemm2BlockN == 0 && (bn == 256 || epi != kEpiQkv) &&
-      pair_tiles >= 40) {
-    // B maps: index k holds box rows bn >> k; the 2-SM kernel loads 128-row halves
-    const CUtensorMap& half = tb3[bn == 256 ? 1 : 0];
+  GemmArgs a = a_in;
+  a.l2_hints = g_gemm_hints;
+  // Chunks of more than 128 rows run on CTA pairs (cta_group::2): the pair's
+  // MMA is M = 256 x N = bn, each CTA receiving its 128 rows of A and bn/2 rows
+  // of the weight tile (24 KB per 64-deep k-block at bn = 128 instead of the
+  // 1-SM tile's 32 KB: the M = 512 projections are bound by L2 -> SM delivery).
+  // At M = 512: QKV / gate-up 48 / 224 pair tiles of N 256. O / down stay on
+  // 1-SM 128 x 128 tiles: measured faster than pairs of N 128 (tools/gemm_sweep.py).
+  if (bn == 192) {
+    if (a.M <= kGemmBlockM || a.N % bn) return fail(CAKE_EINVAL, "gemm: N-192 tiles need M > 128 and N %% 192 == 0");
     switch (epi) {
-      case kEpiBf16: return launch_gemm2<kEpiBf16>(ta, half, a, s);
-      case kEpiF32: return launch_gemm2<kEpiF32>(ta, half, a, s);
-      case kEpiResid: return launch_gemm2<kEpiResid>(ta, half, a, s);
-      case kEpiSwiglu: return launch_gemm2<kEpiSwiglu>(ta, half, a, s);
-      case kEpiQkv: return launch_gemm2<kEpiQkv>(ta, half, a, s);
+      case kEpiBf16: return launch_gemm2<192, kEpiBf16>(ta, tb3[1], a, s);
+      case kEpiF32: return launch_gemm2<192, kEpiF32>(ta, tb3[1], a, s);
+      case kEpiResid: return launch_gemm2<192, kEpiResid>(ta, tb3[1], a, s);
+    }
+    return fail(CAKE_EINVAL, "gemm: unsupported epi %d for N-192 tiles", epi);
+  }
+  if (g_gemm_2sm && a.M > kGemmBlockM && a.N % bn == 0 && (bn == 256 || g_gemm_2sm_n128)) {
+    // B maps: index k holds box rows bn >> k; the pair kernel loads bn/2-row halves
+    const CUtensorMap& half = tb3[1];
+    if (bn == 256) {
+      switch (epi) {
+        case kEpiBf16: return launch_gemm2<256, kEpiBf16>(ta, half, a, s);
+        case kEpiF32: return launch_gemm2<256, kEpiF32>(ta, half, a, s);
+        case kEpiResid: return launch_gemm2<256, kEpiResid>(ta, half, a, s);
+        case kEpiSwiglu: return launch_gemm2<256, kEpiSwiglu>(ta, half, a, s);
+        case kEpiQkv: return launch_gemm2<256, kEpiQkv>(ta, half, a, s);
+      }
+    } else if (epi != kEpiSwiglu) {
+      switch (epi) {
+        case kEpiBf16: return launch_gemm2<128, kEpiBf16>(ta, half, a, s);
+        case kEpiF32: return launch_gemm2<128, kEpiF32>(ta, half, a, s);
+        case kEpiResid: return launch_gemm2<128, kEpiResid>(ta, half, a, s);
+        case kEpiQkv: return launch_gemm2<128, kEpiQkv>(ta, half, a, s);
+      }
     }
   }
   const CUtensorMap& tb = tb3[cs_index(cluster_size_for(a.M))];
@@ -391,6 +415,7 @@ struct cake_model {
   int max_splits = 16;
   size_t part_rows_cap = 0;  // splits * chunk rows * local q heads the partials hold
   float* tp_buf = nullptr;  // fp32 partial sums for the TP all-reduce
+  float* ss = nullptr;      // fused RMSNorm: [H / 128][rows_cap] partial sums of squares of the residual rows
   unsigned* q8_ws = nullptr;  // quant8 encode: ordered min/max keys
   CUtensorMap a_xn, a_attn, a_act;
   CUtensorMap tm_q, tm_kv;  // attention: Q rows of a GQA group, paged K/V pool
@@ -695,6 +720,27 @@ int last_token_pass(cake_model* m, const int32_t* d_token, long long T, const in
   return CAKE_OK;
 }
 
+// RMSNorm folded into the projections (gemm.cuh GemmArgs): the residual
+// epilogues of O / down write bf16(h) and per-tile sums of squares, the next
+// QKV / gate-up epilogue applies the row scale. Single-GPU only (the TP path
+// adds the all-reduced partials in a separate kernel and keeps rmsnorm).
+// CAKE_FUSED_NORM=0 restores the standalone kernel (A/B measurements).
+bool fused_norm(const cake_model* m) {
+  static const bool on = [] {
+    const char* e = std::getenv("CAKE_FUSED_NORM");
+    return !(e && e[0] == '0');
+  }();
+  return on && m->cfg.tp_size == 1 && !m->emulated_tp && m->H % 128 == 0;
+}
+
+void set_norm_consumer(cake_model* m, GemmArgs& g) {
+  g.ss_in = m->ss;
+  g.ss_parts = m->H / 128;
+  g.ss_ld = m->rows_cap;
+  g.rms_dim = m->H;
+  g.rms_eps = m->cfg.rms_eps;
+}
+
 int rmsnorm(cake_model* m, const bf16* gamma, long long row0, int rows, const int32_t* abort_flag, cudaStream_t s) {
   ProfScope ps(m, CAKE_K_RMSNORM, s, 0.0, static_cast<double>(rows) * m->H * 6);
   CK(launch_chain(rmsnorm_kernel, dim3((rows + kNormRowsPerCta - 1) / kNormRowsPerCta),
@@ -717,6 +763,11 @@ int row_parallel(cake_model* m, int kind, const CUtensorMap& ta, const CUtensorM
   if (m->cfg.tp_size == 1) {
     g.resid = m->h;
     g.ldr = m->H;
+    if (fused_norm(m)) {
+      g.xb_out = m->xn;
+      g.ss_out = m->ss;
+      g.ss_ld = m->rows_cap;
+    }
     ProfScope ps(m, kind, s, flops, bytes);
     return gemm_dispatch(128, kEpiResid, ta, tb, g, s);
   }
@@ -748,9 +799,11 @@ int layer_attention_half(cake_model* m, int l, long long chunk_start, int M, con
                          const int32_t* d_abort, bool no_kv, cudaStream_t s) {
   const int H = m->H;
   LayerWeights& lw = m->layers[l];
-  CKS(rmsnorm(m, lw.ln1, 0, M, d_abort, s));
+  const bool fused = fused_norm(m) && l > 0;  // layer 0's input is the embedding (no producer epilogue)
+  if (!fused) CKS(rmsnorm(m, lw.ln1, 0, M, d_abort, s));
   {
     GemmArgs g{};
+    if (fused) set_norm_consumer(m, g);
     g.M = M;
     g.N = no_kv ? m->nq * m->hd : m->qkv_rows;
     g.K = H;
@@ -777,9 +830,11 @@ int layer_attention_half(cake_model* m, int l, long long chunk_start, int M, con
 int layer_mlp_half(cake_model* m, int l, int M, const int32_t* d_abort, cudaStream_t s) {
   const int H = m->H;
   LayerWeights& lw = m->layers[l];
-  CKS(rmsnorm(m, lw.ln2, 0, M, d_abort, s));
+  const bool fused = fused_norm(m);
+  if (!fused) CKS(rmsnorm(m, lw.ln2, 0, M, d_abort, s));
   {
     GemmArgs g{};
+    if (fused) set_norm_consumer(m, g);
     g.M = M;
     g.N = 2 * m->F;
     g.K = H;
@@ -929,7 +984,7 @@ int cake_model_destroy(cake_model* m) {
                   static_cast<void*>(m->rope), static_cast<void*>(m->h), static_cast<void*>(m->xn),
                   static_cast<void*>(m->q), static_cast<void*>(m->attn), static_cast<void*>(m->act),
                   static_cast<void*>(m->part_o), static_cast<void*>(m->part_lse),
-                  static_cast<void*>(m->tp_buf), static_cast<void*>(m->q8_ws)})
+                  static_cast<void*>(m->tp_buf), static_cast<void*>(m->q8_ws), static_cast<void*>(m->ss)})
     if (p) cudaFree(p);
   for (auto& p : m->prof) {
     cudaEventDestroy(p.a);
@@ -1072,6 +1127,7 @@ int cake_model_create(const cake_model_config* cfg, cake_model** out) {
   const size_t R = m->rows_cap;
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->h), R * H * sizeof(float)))) return bail(st);
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->xn), R * H * sizeof(bf16)))) return bail(st);
+  if ((st = alloc_dev(reinterpret_cast<void**>(&m->ss), R * ((H + 127) / 128) * sizeof(float)))) return bail(st);
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->q), R * m->nq * hd * sizeof(bf16)))) return bail(st);
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->attn), R * m->nq * hd * sizeof(bf16)))) return bail(st);
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->act), R * F * sizeof(bf16)))) return bail(st);
@@ -1361,7 +1417,10 @@ int cake_kv_encode_q8(cake_model* m, const void* d_chunk, int chunk_len, void* d
 
 int cake_gemm_set_schedule(int schedule) {
   // bit 0: stream-K; bit 1: disable the 2-SM kernel; bit 2: 1-SM weight multicast clusters
-  if (schedule < 0 || schedule > 7) return fail(CAKE_EINVAL, "schedule bits: 1 stream-K, 2 no-2SM, 4 multicast");
+  if (schedule < 0 || schedule > 63)
+    return fail(CAKE_EINVAL, "schedule bits: 1 stream-K, 2 no-2SM, 4 multicast, 8 2-SM for N-128 tiles");
+  g_gemm_2sm_n128 = (schedule & 8) ? 1 : 0;
+  g_gemm_hints = 3 ^ ((schedule >> 4) & 3);  // bits 4/5 drop the evict_last hint of A / B
   g_gemm_schedule = schedule & 1;
   g_gemm_2sm = (schedule & 2) ? 0 : 1;
   g_gemm_cluster = (schedule & 4) ? 1 : 0;

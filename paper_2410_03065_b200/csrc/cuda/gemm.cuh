@@ -66,7 +66,22 @@ struct GemmArgs {
   int epoch;
   int whole_tiles;          // 1: classic persistent schedule (tile t -> CTA t % grid), no splits
   int cs;                   // cluster size = CTAs sharing (multicasting) each weight k-block, one m-block each
+  // RMSNorm folded into the projections. Producer side (kEpiResid): besides
+  // h += acc, write bf16(h) (the next projection's A operand) and this tile's
+  // per-row partial sum of squares. Consumer side (any other epilogue): the
+  // row scale rsqrt(sum(partials) / rms_dim + eps) multiplies the accumulator
+  // (norm(x) W^T = rsqrt(ms(x)) * (x W^T) row-wise; gamma = 1 in this model).
+  __nv_bfloat16* xb_out;    // producer: [M, N] bf16 copy of the updated residual (nullptr: off)
+  float* ss_out;            // producer: [num_n_blocks][ss_ld] partial sums of squares
+  const float* ss_in;       // consumer: partials to reduce (nullptr: A is already normalised)
+  int ss_parts, ss_ld, rms_dim;
+  float rms_eps;
+  int l2_hints;             // experiment: bit 0 A evict_last, bit 1 B evict_last (else evict_normal)
 };
+
+__device__ __forceinline__ uint64_t gemm_policy(int hints, int bit) {
+  return (hints >> bit) & 1 ? policy_evict_last() : policy_evict_normal();
+}
 
 constexpr int kGemmBlockM = 128;
 constexpr int kGemmBlockK = 64;  // 64 bf16 = one 128-B swizzle row
@@ -120,6 +135,31 @@ struct StreamK {
   }
 };
 
+// Epilogue inputs that do not depend on the accumulator, loaded by the
+// epilogue warps BEFORE they wait for it (they are idle during the tile's
+// mainloop, and at M = 512 most CTAs own a single tile, so anything loaded
+// after the wait is exposed): the residual rows this thread will update
+// (kEpiResid, <= 128 columns: 128 registers) and the fused-RMSNorm row scale.
+template <int BLOCK_N, int EPI>
+struct EpiPre {
+  static constexpr bool kH = (EPI == kEpiResid) && BLOCK_N <= 128;
+  float4 h[kH ? BLOCK_N / 4 : 1];
+  float rs = 1.f;
+  __device__ __forceinline__ void load(const GemmArgs& a, int m, int n_blk, bool partial) {
+    if (partial || m >= a.M) return;
+    if (a.ss_in != nullptr) {
+      float t = 0.f;
+      for (int p = 0; p < a.ss_parts; ++p) t += __ldcg(a.ss_in + static_cast<size_t>(p) * a.ss_ld + m);
+      rs = rsqrtf(t / static_cast<float>(a.rms_dim) + a.rms_eps);
+    }
+    if constexpr (kH) {
+      const float4* src = reinterpret_cast<const float4*>(a.resid + static_cast<size_t>(m) * a.ldr + n_blk * BLOCK_N);
+#pragma unroll
+      for (int q = 0; q < BLOCK_N / 4; ++q) h[q] = src[q];
+    }
+  }
+};
+
 // Fused epilogue of one accumulator tile: this thread owns TMEM lane `row`
 // (output row m). partial: publish the fp32 tile into workspace slot my_slot
 // and raise its flag; otherwise wait for n_parts partial slots (first_slot +
@@ -127,7 +167,7 @@ struct StreamK {
 template <int BLOCK_N, int EPI>
 __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t tbase, int row, int m, int n_blk,
                                               bool partial, int my_slot, int first_slot, int n_parts,
-                                              int slot_stride, int ep_tid) {
+                                              int slot_stride, int ep_tid, const EpiPre<BLOCK_N, EPI>& pre) {
   const bool valid = m < args.M;
   if (partial) {
     // ---- partial segment: publish the fp32 tile in this CTA's slot
@@ -147,6 +187,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t tba
     if (ep_tid == 0) atomicExch(args.sk_flags + my_slot, args.epoch);
   } else {
     // ---- full tile, or the k = 0 owner of a split tile: wait for the other parts
+    const float rs = pre.rs;  // fused RMSNorm row scale (consumer side)
     if (n_parts > 0) {
       if (ep_tid == 0) {
         for (int p = 0; p < n_parts; ++p)
@@ -165,10 +206,15 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t tba
 #pragma unroll
         for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) + __ldcg(part + i * kGemmBlockM));
       }
+      if (args.ss_in != nullptr) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * rs);
+      }
     };
 
     if constexpr (EPI == kEpiBf16 || EPI == kEpiF32 || EPI == kEpiResid) {
-#pragma unroll 1
+      float ss = 0.f;  // kEpiResid: this row's sum of squares over the tile's columns
+#pragma unroll
       for (int c = 0; c < BLOCK_N / 32; ++c) {
         uint32_t r[32];
         load_acc(c * 32, r);
@@ -195,17 +241,38 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t tba
           } else {
             float4* dst =
                 reinterpret_cast<float4*>(args.resid + static_cast<size_t>(m) * args.ldr + n0);
+            float4 hv[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              float4 h = dst[q];
+              if constexpr (EpiPre<BLOCK_N, EPI>::kH)
+                hv[q] = pre.h[c * 8 + q];
+              else
+                hv[q] = dst[q];
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 h = hv[q];
               h.x += __uint_as_float(r[q * 4]);
               h.y += __uint_as_float(r[q * 4 + 1]);
               h.z += __uint_as_float(r[q * 4 + 2]);
               h.w += __uint_as_float(r[q * 4 + 3]);
               dst[q] = h;
+              hv[q] = h;
+              ss += h.x * h.x + h.y * h.y + h.z * h.z + h.w * h.w;
+            }
+            if (args.xb_out != nullptr) {
+              __nv_bfloat16* xb = args.xb_out + static_cast<size_t>(m) * args.ldr + n0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                st_global_v4(xb + q * 8, pack_bf16(hv[2 * q].x, hv[2 * q].y), pack_bf16(hv[2 * q].z, hv[2 * q].w),
+                             pack_bf16(hv[2 * q + 1].x, hv[2 * q + 1].y),
+                             pack_bf16(hv[2 * q + 1].z, hv[2 * q + 1].w));
             }
           }
         }
+      }
+      if constexpr (EPI == kEpiResid) {
+        if (args.ss_out != nullptr && valid) args.ss_out[static_cast<size_t>(n_blk) * args.ss_ld + m] = ss;
       }
     } else if constexpr (EPI == kEpiSwiglu) {
       static_assert(BLOCK_N == 256, "gate/up interleave is 128 columns");
@@ -367,7 +434,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
-      const uint64_t pol_w = policy_evict_last();   // weights: reused by the other m-blocks
+      const uint64_t pol_w = gemm_policy(args.l2_hints, 1);  // weights: reused by the other m-blocks
+      const uint64_t pol_a = gemm_policy(args.l2_hints, 0);
       StreamK sk(units, nk, cluster, n_clusters, args.whole_tiles);
       int stage = 0;
       uint32_t phase = 0;
@@ -378,8 +446,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
-          tma_load_2d(smem_a + stage * Cfg::kABytes, &tmap_a, &full_bar[stage], kb * kGemmBlockK,
-                      m_blk * kGemmBlockM);
+          tma_load_2d_hint(smem_a + stage * Cfg::kABytes, &tmap_a, &full_bar[stage], kb * kGemmBlockK,
+                           m_blk * kGemmBlockM, pol_a);
           if (cs > 1)
             tma_load_2d_mc(smem_b + stage * Cfg::kBBytes + rank * b_rows * 128, &tmap_b, &full_bar[stage],
                            kb * kGemmBlockK, n_blk * BLOCK_N + rank * b_rows, mc_mask, pol_w);
@@ -444,6 +512,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int m_blk = (tile % m_groups) * cs + rank;
       const int n_blk = tile / m_groups;
       const int m = m_blk * kGemmBlockM + row;
+      EpiPre<BLOCK_N, EPI> pre;
+      pre.load(args, m, n_blk, kb0 > 0);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase =
@@ -458,7 +528,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           n_parts = sk.cta_of(u_tile + nk - 1) - first_part + 1;
         }
         gemm_epilogue<BLOCK_N, EPI>(args, tbase, row, m, n_blk, partial, blockIdx.x, first_part * cs + rank, n_parts,
-                                    cs, ep_tid);
+                                    cs, ep_tid, pre);
       }
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);

@@ -23,24 +23,23 @@
 
 namespace cake_dev {
 
-constexpr int kGemm2BlockN = 256;
-
+template <int BLOCK_N>
 struct Gemm2Cfg {
+  static_assert(BLOCK_N % 32 == 0 && BLOCK_N >= 64 && BLOCK_N <= 256, "cta_group::2 tile N");
   static constexpr int kABytes = kGemmBlockM * kGemmBlockK * 2;            // this CTA's 128 rows of A
-  static constexpr int kBBytes = (kGemm2BlockN / 2) * kGemmBlockK * 2;     // this CTA's 128 rows of B
+  static constexpr int kBBytes = (BLOCK_N / 2) * kGemmBlockK * 2;          // this CTA's BLOCK_N/2 rows of B
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (200 * 1024) / kStageBytes;               // 6
-  static constexpr int kTmemCols = 512;                                    // 2 x 256-column accumulators
+  static constexpr int kStages = (200 * 1024) / kStageBytes;               // 6 (N 256) .. 8 (N 128)
+  static constexpr int kTmemCols = (2 * BLOCK_N <= 256) ? 256 : 512;       // 2 accumulators
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 };
 
-template <int EPI>
+template <int BLOCK_N, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm2_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                     const GemmArgs args) {
-  using Cfg = Gemm2Cfg;
+  using Cfg = Gemm2Cfg<BLOCK_N>;
   constexpr int kStages = Cfg::kStages;
-  constexpr int BLOCK_N = kGemm2BlockN;
   extern __shared__ uint8_t smem_raw[];
   __shared__ int s_abort;
 
@@ -98,8 +97,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer (both CTAs)
-      const uint64_t pol_w = policy_evict_last();
-      const uint64_t pol_a = policy_evict_last();
+      const uint64_t pol_w = gemm_policy(args.l2_hints, 1);
+      const uint64_t pol_a = gemm_policy(args.l2_hints, 0);
       StreamK sk(units, nk, pair, n_pairs, args.whole_tiles);
       int stage = 0;
       uint32_t phase = 0;
@@ -165,6 +164,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     while (sk.next(tile, kb0, kb1)) {
       const int m = (tile % m_pairs) * 256 + static_cast<int>(rank) * 128 + row;
       const int n_blk = tile / m_pairs;
+      EpiPre<BLOCK_N, EPI> pre;
+      pre.load(args, m, n_blk, kb0 > 0);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase =
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         n_parts = sk.cta_of(u_tile + nk - 1) - first_part + 1;
       }
       gemm_epilogue<BLOCK_N, EPI>(args, tbase, row, m, n_blk, partial, blockIdx.x,
-                                  first_part * 2 + static_cast<int>(rank), n_parts, 2, ep_tid);
+                                  first_part * 2 + static_cast<int>(rank), n_parts, 2, ep_tid, pre);
       tc_fence_before();
       mbar_arrive_cluster(leader_tempty0 + acc * 8);
       if (++acc == 2) {

@@ -7,10 +7,10 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 lib = ctypes.CDLL(os.path.join(ROOT, "paper_2410_03065_b200/_lib/libcake_cuda.so"))
 lib.cake_gemm.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 5 + [ctypes.c_void_p]
-for sched in (0, 2):
+for sched in (2, 8):
     lib.cake_gemm_set_schedule(sched)
-    for (M, N, bn) in [(512, 6144, 256), (512, 4096, 128)]:
-        for K in (64, 256, 1024, 4096):
+    for (M, N, bn) in [(512, 4096, 128)]:
+        for K in (64, 256, 1024, 2048, 4096, 8192):
             a = torch.randn(M, K, device="cuda").bfloat16()
             b = torch.randn(N, K, device="cuda").bfloat16()
             c = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)

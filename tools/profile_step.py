@@ -14,10 +14,11 @@ sched = os.environ.get("GEMM_SCHED")
 if sched is not None:
     from paper_2410_03065_b200 import native
     native.load_cuda().cake_gemm_set_schedule(int(sched))
-rt = GpuRuntime("llama3_8b", max_tokens=T, max_chunk=512)
-tier = rt.build_cache_tier(T, 512, 42)
+C = int(os.environ.get("C", "512"))
+rt = GpuRuntime("llama3_8b", max_tokens=T, max_chunk=C)
+tier = rt.build_cache_tier(T, C, 42)
 for i in range(int(os.environ.get("REPS", "2"))):
     t0 = time.time()
-    r = rt.run(tier, T, 512, 42, mbps=64000, mode=mode)
-    print(f"{mode} T={T}: device {r.device_ttft_ms:.2f} ms, wall {1e3*(time.time()-t0):.1f} ms, "
+    r = rt.run(tier, T, C, 42, mbps=float(os.environ.get("MBPS", "64000")), mode=mode)
+    print(f"{mode} T={T} C={C}: device {r.device_ttft_ms:.2f} ms, wall {1e3*(time.time()-t0):.1f} ms, "
           f"launches {r.kernel_launches}, merge {r.merge_point}", flush=True)
