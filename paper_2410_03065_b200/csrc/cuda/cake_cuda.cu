@@ -18,6 +18,7 @@
 
 #include "attention.cuh"
 #include "attention_tc.cuh"
+#include "attention_fa4.cuh"
 #include "cake_cuda.h"
 #include "elementwise.cuh"
 #include "gemm.cuh"
@@ -419,7 +420,8 @@ struct cake_model {
   unsigned* q8_ws = nullptr;  // quant8 encode: ordered min/max keys
   CUtensorMap a_xn, a_attn, a_act;
   CUtensorMap tm_q, tm_kv;  // attention: Q rows of a GQA group, paged K/V pool
-  int attn_impl = 0;        // 0 tcgen05 (product), 1 mma.sync (cross-check)
+  int attn_impl = 0;        // 0 product dispatch, 1 mma.sync (cross-check), 2 one-tile / 3 two-tile tcgen05 only
+  int* attn_tickets = nullptr;  // split arrival tickets of the two-tile kernel (zero at rest)
   ncclComm_t comm = nullptr;
   bool emulated_tp = false;  // test driver sums the ranks' partials itself (cake_prefill_group)
   unsigned profile_mask = 0;  // bit k: bracket launches of kernel class k with events
@@ -512,10 +514,85 @@ enum { kWq = 0, kWk = 1, kWv = 2, kWo = 3, kWgate = 4, kWup = 5, kWdown = 6 };
 
 namespace {
 
+constexpr long long kFa4MinPrefix = 8192;  // measured crossover of the two attention kernels
+long long* g_fa4_trace = nullptr;  // debug: clock stamps of one CTA (cake_debug_fa4_trace)
+int g_fa4_trace_layer = -1;
+
+// Two-tile tcgen05 attention (attention_fa4.cuh): 2 x 128 (token, head) rows
+// of one KV head per CTA; splits of the prefix fill one wave of SMs, the last
+// split of each tile pair combines in split order (no combine kernel).
+int attention_fa4(cake_model* m, long long chunk_start, int chunk_len, int layer, const int32_t* bt,
+                  const int32_t* abort_flag, cudaStream_t s) {
+  const int G = m->nq / m->nkv;
+  const int pair_tokens = 2 * (128 / G);
+  const int qpairs = (chunk_len + pair_tokens - 1) / pair_tokens;
+  const long long kv_end = chunk_start + chunk_len;
+  const int n_pages = static_cast<int>((kv_end + kAttnPage - 1) / kAttnPage);
+  const int base_ctas = qpairs * m->nkv;
+  // partial slots: 2 tiles x 128 rows x hd fp32 per (split, tile pair, KV head)
+  const int cap = static_cast<int>(m->part_rows_cap / (static_cast<size_t>(base_ctas) * 256));
+  const int splits =
+      std::max(1, std::min({num_sms() / std::max(1, base_ctas), std::max(1, n_pages / 4), m->max_splits, cap}));
+  const double vis = static_cast<double>(chunk_len) * chunk_start + 0.5 * chunk_len * (chunk_len + 1.0);
+  const double flops = 4.0 * m->hd * m->nq * vis;
+  const double bytes = static_cast<double>(kv_end) * m->nkv * m->hd * 2 * 2 + 2.0 * chunk_len * m->nq * m->hd * 2;
+  ProfScope ps(m, CAKE_K_ATTN, s, flops, bytes);
+  F4Args fa{};
+  fa.fa.q = m->q;
+  fa.fa.block_table = bt;
+  fa.fa.out = m->attn;
+  fa.fa.part_o = m->part_o;
+  fa.fa.part_lse = m->part_lse;
+  fa.fa.chunk_start = chunk_start;
+  fa.fa.chunk_len = chunk_len;
+  fa.fa.n_q_heads = m->nq;
+  fa.fa.n_kv_heads = m->nkv;
+  fa.fa.layer = layer;
+  fa.fa.n_layers = m->L;
+  fa.fa.num_splits = splits;
+  fa.fa.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(m->hd));
+  fa.fa.abort_flag = abort_flag;
+  fa.tickets = m->attn_tickets;
+  fa.trace = (g_fa4_trace_layer == layer) ? g_fa4_trace : nullptr;
+  const dim3 grid(qpairs, m->nkv, splits);
+  if (m->hd == 128) {
+    static bool cfgd = false;
+    if (!cfgd) {
+      CK(cudaFuncSetAttribute(attn_fa4_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, F4Cfg<128>::kSmem));
+      cfgd = true;
+    }
+    const cudaError_t e = launch_chain(attn_fa4_kernel<128>, grid, dim3(kF4Threads), F4Cfg<128>::kSmem, s, 1,
+                                       m->tm_q, m->tm_kv, fa);
+    if (e != cudaSuccess) {
+      cudaFuncAttributes fa_attr{};
+      cudaFuncGetAttributes(&fa_attr, attn_fa4_kernel<128>);
+      return fail(CAKE_ECUDA + static_cast<int>(e), "attn_fa4_kernel<128>: %s (regs %d, max threads %d, static smem %zu, "
+                  "dynamic %d, max dynamic %d)", cudaGetErrorString(e), fa_attr.numRegs, fa_attr.maxThreadsPerBlock,
+                  fa_attr.sharedSizeBytes, F4Cfg<128>::kSmem, fa_attr.maxDynamicSharedSizeBytes);
+    }
+  } else if (m->hd == 64) {
+    static bool cfgd = false;
+    if (!cfgd) {
+      CK(cudaFuncSetAttribute(attn_fa4_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, F4Cfg<64>::kSmem));
+      cfgd = true;
+    }
+    CK(launch_chain(attn_fa4_kernel<64>, grid, dim3(kF4Threads), F4Cfg<64>::kSmem, s, 1, m->tm_q, m->tm_kv, fa));
+  } else {
+    return fail(CAKE_EINVAL, "attention: head_dim %d unsupported", m->hd);
+  }
+  return CAKE_OK;
+}
+
 int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, const int32_t* bt,
               const int32_t* abort_flag, cudaStream_t s) {
+  // Product dispatch (impl 0): the two-tile kernel once the prefix is long
+  // (its per-key cost is ~12% lower, tools/attn_ab.py) and the one-tile kernel
+  // for short prefixes and the 1-token step (the two-tile kernel's split
+  // combine and 2 x 128-row tiles cost more than they save there).
+  if ((m->attn_impl == 0 && chunk_start >= kFa4MinPrefix && chunk_len >= 128) || m->attn_impl == 3)
+    return attention_fa4(m, chunk_start, chunk_len, layer, bt, abort_flag, s);
   const int G = m->nq / m->nkv;
-  const bool tc = m->attn_impl == 0;
+  const bool tc = m->attn_impl != 1;
   const int rows_per_cta = tc ? kFaRows : kAttnRows;
   const int tok_per_tile = rows_per_cta / G;
   const int qtiles = (chunk_len + tok_per_tile - 1) / tok_per_tile;
@@ -984,7 +1061,8 @@ int cake_model_destroy(cake_model* m) {
                   static_cast<void*>(m->rope), static_cast<void*>(m->h), static_cast<void*>(m->xn),
                   static_cast<void*>(m->q), static_cast<void*>(m->attn), static_cast<void*>(m->act),
                   static_cast<void*>(m->part_o), static_cast<void*>(m->part_lse),
-                  static_cast<void*>(m->tp_buf), static_cast<void*>(m->q8_ws), static_cast<void*>(m->ss)})
+                  static_cast<void*>(m->tp_buf), static_cast<void*>(m->q8_ws), static_cast<void*>(m->ss),
+                  static_cast<void*>(m->attn_tickets)})
     if (p) cudaFree(p);
   for (auto& p : m->prof) {
     cudaEventDestroy(p.a);
@@ -1136,6 +1214,8 @@ int cake_model_create(const cake_model_config* cfg, cake_model** out) {
   m->max_splits = 64;
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->part_o), m->part_rows_cap * hd * sizeof(float)))) return bail(st);
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->part_lse), m->part_rows_cap * sizeof(float)))) return bail(st);
+  if ((st = alloc_dev(reinterpret_cast<void**>(&m->attn_tickets), R * m->nkv * sizeof(int)))) return bail(st);
+  cudaMemset(m->attn_tickets, 0, R * m->nkv * sizeof(int));
   if (c.tp_size > 1 && (st = alloc_dev(reinterpret_cast<void**>(&m->tp_buf), R * H * sizeof(float))))
     return bail(st);
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->q8_ws), 2 * sizeof(unsigned)))) return bail(st);
@@ -1198,8 +1278,18 @@ int cake_nccl_destroy(void* comm) {
   return CAKE_OK;
 }
 
+// Debug: record clock64 stamps of CTA (0,0,0) of the two-tile attention kernel
+// at `layer` into dev_buf (>= 64 + 2*64*8 int64), nullptr to stop.
+CAKE_API int cake_debug_fa4_trace(void* dev_buf, int layer) {
+  g_fa4_trace = static_cast<long long*>(dev_buf);
+  g_fa4_trace_layer = layer;
+  return CAKE_OK;
+}
+
 int cake_model_set_attention_impl(cake_model* m, int impl) {
-  if (impl != 0 && impl != 1) return fail(CAKE_EINVAL, "attention impl must be 0 (tcgen05) or 1 (mma.sync)");
+  if (impl < 0 || impl > 3)
+    return fail(CAKE_EINVAL, "attention impl must be 0 (product dispatch), 1 (mma.sync), 2 (one-tile tcgen05) "
+                             "or 3 (two-tile tcgen05)");
   m->attn_impl = impl;
   return CAKE_OK;
 }

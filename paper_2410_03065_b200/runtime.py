@@ -134,8 +134,10 @@ class GpuRuntime:
         return out.raw
 
     def set_attention_impl(self, impl: str):
-        """"tcgen05" (product path) or "mma_sync" (independent cross-check kernel)."""
-        self.n.call("cake_gpu_set_attention_impl", self.h, {"tcgen05": 0, "mma_sync": 1}[impl])
+        """"tcgen05" (product dispatch), "tcgen05_1tile" / "tcgen05_2tile" (one tcgen05
+        kernel for every chunk) or "mma_sync" (independent cross-check kernel)."""
+        self.n.call("cake_gpu_set_attention_impl", self.h,
+                    {"tcgen05": 0, "mma_sync": 1, "tcgen05_1tile": 2, "tcgen05_2tile": 3}[impl])
 
     def set_profiling(self, kernels="all"):
         """Bracket launches of the named kernel classes with CUDA events ("all", None, or a list)."""

@@ -31,13 +31,16 @@ def gpu():
         pytest.skip("no GPU")
 
 
-def test_8b_two_layers_vs_oracle(gpu):
+@pytest.mark.parametrize("impl", ["tcgen05", "tcgen05_2tile"])
+def test_8b_two_layers_vs_oracle(gpu, impl):
+    """Product dispatch, and the two-tile attention kernel forced for every chunk."""
     import llama_oracle
     from paper_2410_03065_b200.cake import Cake
     from paper_2410_03065_b200.runtime import GpuRuntime
 
     T, C, seed = 1024, 512, 7
     rt = GpuRuntime("llama3_8b", n_layers=2, max_tokens=T, max_chunk=C)
+    rt.set_attention_impl(impl)
     tier = rt.build_cache_tier(T, C, seed)
     dims = (2,) + DIMS[1:]
     toks = Cake().token_stream(seed, T).astype(np.int32)
