@@ -75,6 +75,7 @@ typedef struct cake_run_opts {
   uint32_t jitter_max_us;
   uint64_t jitter_seed;
   int race_to_finish; /* B200 extension */
+  int cached_prefix;  /* B200 extension: the tier may hold only a leading run of chunks */
 } cake_run_opts;
 
 typedef struct cake_summary {

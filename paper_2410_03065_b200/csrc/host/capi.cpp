@@ -67,8 +67,10 @@ RunOptions to_opts(const cake_run_opts* o) {
   r.jitter_seed = o->jitter_seed;
 #ifndef CAKE_REFERENCE_BUILD
   r.race_to_finish = o->race_to_finish != 0;
+  r.cached_prefix = o->cached_prefix != 0;
 #else
   if (o->race_to_finish) throw std::invalid_argument("race_to_finish is a B200 extension");
+  if (o->cached_prefix) throw std::invalid_argument("cached_prefix is a B200 extension");
 #endif
   return r;
 }
@@ -202,6 +204,7 @@ void cake_run_opts_default(cake_run_opts* o) {
   o->jitter_max_us = d.jitter_max_us;
   o->jitter_seed = d.jitter_seed;
   o->race_to_finish = 0;
+  o->cached_prefix = 0;
 }
 
 int cake_sim_run(uint32_t n, const uint64_t* token_starts, const uint32_t* token_counts, const uint64_t* encoded_bytes,

@@ -692,8 +692,10 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
                        double power, const RunOptions& opt) {
   GpuContext::Impl& g = *opt.gpu->impl();
   if (codec.kind == Codec::Kind::factor) throw std::invalid_argument("gpu run: the factor codec models bytes only");
-  const auto n = static_cast<std::uint32_t>(plan.chunks.size());
+  const auto n = static_cast<std::uint32_t>(plan.chunks.size());  // the cached prefix: bidirectional phase
+  const auto n_all = static_cast<std::uint32_t>(n + plan.suffix.size());
   check_chunking(g, plan.chunks, tokens.size());
+  check_chunking(g, plan.suffix, tokens.size());
   for (std::uint32_t i = 0; i < n; ++i) {
     const auto raw = static_cast<std::uint64_t>(cake_kv_chunk_bytes(g.model, plan.chunks[i].token_count));
     if (plan.encoded_bytes[i] != codec.encoded_size(raw))
@@ -703,9 +705,10 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   const bool compute_on = mode == RunMode::compute_only || (mode == RunMode::cake && opt.compute_enabled);
   if (!io_on && !compute_on) throw std::invalid_argument("run: no side enabled");
   TpCoordinator* tp = g.tp.get();
+  if (tp && !plan.suffix.empty()) throw std::invalid_argument("gpu run: partially cached prompts are single-GPU only");
   if (tp && !tp->leader()) return run_follower(g, *tp, plan, tokens, trace, store, mode, opt);
   const bool race = opt.race_to_finish && io_on && compute_on && tp == nullptr;  // TP: boundary race not mirrored yet
-  g.ensure_events(n);
+  g.ensure_events(n_all);
   if (tp) tp->begin_run(++g.run_counter, n);
   check(cake_cuda_device_sync(), "pre-run sync");
   long long launches0 = 0;
@@ -750,7 +753,7 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
 
   RunReport rep;
   rep.mode = mode;
-  rep.n_chunks = n;
+  rep.n_chunks = n_all;
   if (compute_on) {
     ComputeEngine engine(cost, TokenBudget{opt.token_budget, power});
     ComputeEngine::ForwardHooks hooks;
@@ -789,8 +792,20 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   // already completed (the commit happens after its event sync), and
   // whatever the copy stream still carries (a lost race) writes pages the
   // final block table does not reference.
-  const ChunkSpec& tail = plan.chunks[n - 1];
-  const bool tail_hidden = run.commit[n - 1].load() == kByCompute && backend.last_launched() == static_cast<int>(n - 1);
+  // ---------------------------------------------------------------- uncached suffix
+  // Every prefix chunk is committed, so the suffix chunks (their prefix
+  // attention reads all of it, through the final block table) run back to
+  // back on the compute stream.
+  for (const ChunkSpec& c : plan.suffix) {
+    check(cake_event_record(g.ev_start[c.index]->h, g.s_compute), "record");
+    check(cake_prefill_chunk(g.model, g.tokens.p + c.token_start, static_cast<long long>(c.token_start),
+                             static_cast<int>(c.token_count), g.final_bt, nullptr, 0, g.s_compute),
+          "suffix prefill");
+    check(cake_event_record(g.ev_end[c.index]->h, g.s_compute), "record");
+  }
+  const ChunkSpec& tail = plan.suffix.empty() ? plan.chunks[n - 1] : plan.suffix.back();
+  const bool tail_hidden = !plan.suffix.empty() || (run.commit[n - 1].load() == kByCompute &&
+                                                    backend.last_launched() == static_cast<int>(n - 1));
   const long long T = static_cast<long long>(tail.token_start + tail.token_count);
   if (tp) tp->publish_final(tail_hidden ? 0 : 1, static_cast<int>(tail.token_count) - 1);
   check(cake_event_record(g.ev_final_start->h, g.s_compute), "record");
@@ -806,9 +821,14 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
     loader->wait();
     rep.chunks.insert(rep.chunks.end(), loader->records().begin(), loader->records().end());
   }
+  for (const ChunkSpec& c : plan.suffix)
+    rep.chunks.push_back({c.index, Side::compute, run.device_time(g.ev_start[c.index]->h),
+                          run.device_time(g.ev_end[c.index]->h), 0});
   detail::finalize_report(rep, 0);
-  rep.merge_point = merge_from_records(rep);
-  rep.computed_fraction = static_cast<double>(rep.merge_point) / n;
+  rep.merge_point = std::min(merge_from_records(rep), n);  // within the cached prefix
+  std::uint32_t computed = 0;
+  for (const ChunkRecord& r : rep.chunks) computed += r.side == Side::compute ? 1u : 0u;
+  rep.computed_fraction = static_cast<double>(computed) / n_all;
 
   info.kv_resident_us = rep.ttft_us;
   float ms = 0.f;

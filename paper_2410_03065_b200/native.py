@@ -32,7 +32,7 @@ class CakeRecord(C.Structure):
 class CakeRunOpts(C.Structure):
     _fields_ = [("compute_enabled", C.c_int), ("io_enabled", C.c_int), ("token_budget", u32),
                 ("throttle_quantum_bytes", u64), ("decode_us_per_byte", dbl), ("jitter_max_us", u32),
-                ("jitter_seed", u64), ("race_to_finish", C.c_int)]
+                ("jitter_seed", u64), ("race_to_finish", C.c_int), ("cached_prefix", C.c_int)]
 
 
 class CakeSummary(C.Structure):

@@ -145,3 +145,26 @@ def test_two_tile_attention_matches_one_tile_kernel(setup):
     for a, b in zip(two, one):
         assert rel(a, b) <= 2e-2
     assert rel(lg_two, lg_one) <= 2e-2
+
+
+@pytest.mark.parametrize("mode", ["cake", "io_only"])
+def test_partially_cached_prompt(setup, mode):
+    """Only a prefix of the prompt is in the tier (cached_prefix): the bidirectional
+    phase covers it, the uncached suffix is computed after it. The assembled cache
+    and the first-token logits are bit-identical to a full compute-only run."""
+    rt, T, C = setup["rt"], setup["T"], setup["C"]
+    rt.run(setup["tier"], T, C, 42, mbps=1000, mode="compute_only")
+    want_kv = [rt.read_chunk(s, C) for s in range(0, T, C)]
+    want = rt.logits()
+    cached = T // 2
+    part = rt.build_cache_tier(cached, C, 42)
+    r = rt.run(part, T, C, 42, mbps=1000, mode=mode, cached_prefix=True)
+    assert r.n_chunks == T // C
+    assert sorted(c.index for c in r.chunks) == list(range(T // C))
+    assert all(c.side == "compute" for c in r.chunks if c.index >= cached // C)
+    assert r.merge_point <= cached // C
+    assert not r.recomputed_last  # the computed suffix holds the last token's hidden state
+    assert [rt.read_chunk(s, C) for s in range(0, T, C)] == want_kv
+    assert np.array_equal(rt.logits(), want)
+    with pytest.raises(Exception):
+        rt.run(part, T, C, 42, mbps=1000, mode=mode)  # without the option a missing chunk is an error

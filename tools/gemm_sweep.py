@@ -16,7 +16,7 @@ lib.cake_gemm.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 5 + [ctypes.c_
 variants = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "0,2,6,1").split(",")]
 names = (sys.argv[2] if len(sys.argv) > 2 else "qkv,o,gu,down").split(",")
 shapes = {"qkv": (512, 6144, 4096, 256), "qkv192": (512, 6144, 4096, 192), "gu192": (512, 28416, 4096, 192), "o": (512, 4096, 4096, 128), "gu": (512, 28672, 4096, 256),
-          "down": (512, 4096, 14336, 128), "o1k": (1024, 4096, 4096, 128), "qkv1k": (1024, 6144, 4096, 256)}
+          "down": (512, 4096, 14336, 128), "o256": (512, 4096, 4096, 256), "down256": (512, 4096, 14336, 256), "o1k": (1024, 4096, 4096, 128), "qkv1k": (1024, 6144, 4096, 256)}
 for name in names:
     M, N, K, bn = shapes[name]
     a = torch.randn(M, K, device="cuda").bfloat16()
