@@ -38,12 +38,9 @@ def t_us(M, N, K, bn, sched):
 
 
 import sys
-cases = []
-cases = [("1-SM 128x128 1 CTA", 128, 128, 128, 2), ("1-SM 128x256 1 CTA", 128, 256, 256, 2),
-         ("2-SM 256x128 1 pair", 256, 128, 128, 8), ("2-SM 256x256 1 pair", 256, 256, 256, 0),
-         ("2-SM 256x128 4 pairs", 256, 512, 128, 8), ("2-SM 256x256 4 pairs", 256, 1024, 256, 0),
-         ("1-SM 128x128 4x32", 512, 4096, 128, 2), ("2-SM 256x128 2x32", 512, 4096, 128, 8),
-         ("2-SM 256x256 2x24", 512, 6144, 256, 0)]
+cases = [("2-SM 2x256 1 pair", 256, 512, 128, 0), ("2-SM 2x256 16 pairs", 512, 4096, 128, 0),
+         ("2-SM 2x256 24 pairs", 512, 6144, 256, 0), ("2-SM 256 48 pairs", 512, 6144, 256, 64),
+         ("1-SM 128x128 128 CTAs", 512, 4096, 128, 64 | 2)]
 for name, M, N, bn, sched in cases:
     t1, t2 = t_us(M, N, 4096, bn, sched), t_us(M, N, 12288, bn, sched)
     per_kb = (t2 - t1) / (8192 / 64)
