@@ -117,10 +117,9 @@ typedef struct cake_model cake_model;
 CAKE_API int cake_model_create(const cake_model_config* cfg, cake_model** out);
 CAKE_API int cake_model_destroy(cake_model* m);
 CAKE_API int cake_model_get_info(const cake_model* m, cake_model_info* out);
-/* Attention kernel variant: 0 = product dispatch (tcgen05/TMEM flash
- * attention: the two-tile kernel for prefixes >= 8K tokens, the one-tile
- * kernel below), 1 = mma.sync flash attention (independent cross-check),
- * 2 / 3 = the one-tile / two-tile tcgen05 kernel for every chunk (tests). */
+/* Attention kernel variant: 0 = product dispatch (the one-tile tcgen05/TMEM
+ * flash attention kernel), 1 = mma.sync flash attention (independent
+ * cross-check), 2 / 3 = the one-tile / two-tile tcgen05 kernel (tests). */
 CAKE_API int cake_model_set_attention_impl(cake_model* m, int impl);
 /* NCCL plumbing for head-sharded TP (one process per GPU): rank 0 makes the
  * 128-byte id, the launcher broadcasts it, every rank inits its communicator. */

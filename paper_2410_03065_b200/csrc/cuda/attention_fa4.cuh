@@ -72,21 +72,6 @@ struct F4Args {
   long long* trace;  // debug (nullptr): clock64 stamps of CTA (0,0,0), see tools/fa4_trace.py
 };
 
-// 2^x for a pair on the FMA pipe (same polynomial as ex2_poly, attention_tc.cuh).
-__device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -125.0f);
-  x.y = fmaxf(x.y, -125.0f);
-  const float2 big = make_float2(12582912.0f, 12582912.0f);
-  const float2 t = fadd2(x, big);
-  const float2 u = fadd2(t, make_float2(-12582912.0f, -12582912.0f));  // round(x)
-  const float2 f = make_float2(x.x - u.x, x.y - u.y);
-  float2 p = ffma2(make_float2(0.05517132f, 0.05517132f), f, make_float2(0.24261054f, 0.24261054f));
-  p = ffma2(p, f, make_float2(0.69326099f, 0.69326099f));
-  p = ffma2(p, f, make_float2(0.99992811f, 0.99992811f));
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
-}
-
 template <int HD>
 __global__ void __launch_bounds__(kF4Threads, 1)
     attn_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,

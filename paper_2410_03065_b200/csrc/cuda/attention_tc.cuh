@@ -81,6 +81,21 @@ __device__ __forceinline__ float ex2_poly(float x) {
   p = fmaf(p, f, 0.99992811f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+// 2^x for a pair on the FMA pipe (ex2_poly on FFMA2 / FADD2).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.0f);
+  x.y = fmaxf(x.y, -125.0f);
+  const float2 big = make_float2(12582912.0f, 12582912.0f);
+  const float2 t = fadd2(x, big);
+  const float2 u = fadd2(t, make_float2(-12582912.0f, -12582912.0f));  // round(x)
+  const float2 f = make_float2(x.x - u.x, x.y - u.y);
+  float2 p = ffma2(make_float2(0.05517132f, 0.05517132f), f, make_float2(0.24261054f, 0.24261054f));
+  p = ffma2(p, f, make_float2(0.69326099f, 0.69326099f));
+  p = ffma2(p, f, make_float2(0.99992811f, 0.99992811f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 // pairs i of the 32 per half-block row whose exponentials go to ex2_poly
 constexpr unsigned kFaPolyPairs = 0x88888888u;  // every 4th pair: 25%
 
@@ -341,20 +356,26 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         m = mx;
       }
       const float nbase = (m == -INFINITY) ? 0.f : -m;
-      float rs0 = 0.f, rs1 = 0.f;
+      const float2 sc2 = make_float2(sc, sc), nb2 = make_float2(nbase, nbase);
+      float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       uint32_t pk[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const bool poly = (kFaPolyPairs >> i) & 1u;
-        const float x0 = fmaf(sv[2 * i], sc, nbase), x1 = fmaf(sv[2 * i + 1], sc, nbase);
-        const float p0 = poly ? ex2_poly(x0) : ex2_approx(x0);
-        const float p1 = poly ? ex2_poly(x1) : ex2_approx(x1);
-        rs0 += p0;
-        rs1 += p1;
-        pk[i] = pack_bf16(p0, p1);
+        const float2 x = ffma2(make_float2(sv[2 * i], sv[2 * i + 1]), sc2, nb2);
+        float2 p;
+        if (poly) {
+          p = ex2_poly2(x);
+        } else {
+          p.x = ex2_approx(x.x);
+          p.y = ex2_approx(x.y);
+        }
+        rs[i & 3] = fadd2(rs[i & 3], p);
+        pk[i] = pack_bf16(p.x, p.y);
       }
       tmem_st32(tS + g * 32, pk);
-      l += rs0 + rs1;
+      const float2 rs01 = fadd2(rs[0], rs[1]), rs23 = fadd2(rs[2], rs[3]);
+      l += (rs01.x + rs23.x) + (rs01.y + rs23.y);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_ready[s]);

@@ -514,7 +514,7 @@ enum { kWq = 0, kWk = 1, kWv = 2, kWo = 3, kWgate = 4, kWup = 5, kWdown = 6 };
 
 namespace {
 
-constexpr long long kFa4MinPrefix = 8192;  // measured crossover of the two attention kernels
+constexpr long long kFa4MinPrefix = 1LL << 62;  // product never picks the two-tile kernel (see attention())
 long long* g_fa4_trace = nullptr;  // debug: clock stamps of one CTA (cake_debug_fa4_trace)
 int g_fa4_trace_layer = -1;
 
@@ -585,10 +585,9 @@ int attention_fa4(cake_model* m, long long chunk_start, int chunk_len, int layer
 
 int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, const int32_t* bt,
               const int32_t* abort_flag, cudaStream_t s) {
-  // Product dispatch (impl 0): the two-tile kernel once the prefix is long
-  // (its per-key cost is ~12% lower, tools/attn_ab.py) and the one-tile kernel
-  // for short prefixes and the 1-token step (the two-tile kernel's split
-  // combine and 2 x 128-row tiles cost more than they save there).
+  // Product dispatch (impl 0) is the one-tile kernel for every chunk: with
+  // FFMA2/FADD2 softmax it is faster than the two-tile kernel at every prefix
+  // measured (up to 32K, tools/attn_ab.py); impl 3 forces the two-tile kernel.
   if ((m->attn_impl == 0 && chunk_start >= kFa4MinPrefix && chunk_len >= 128) || m->attn_impl == 3)
     return attention_fa4(m, chunk_start, chunk_len, layer, bt, abort_flag, s);
   const int G = m->nq / m->nkv;
