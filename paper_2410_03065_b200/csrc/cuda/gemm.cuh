@@ -316,14 +316,17 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t tba
           if (!valid) continue;
           float o0[32], o1[32];
           if (region < 2) {
-            const float2* cs = args.rope + pos * half + j * 32;
+            // (cos, sin) of dims i, i+1 in one 16-B load (rows of hd/2 float2 are 16-B aligned)
+            const float4* cs = reinterpret_cast<const float4*>(args.rope + pos * half + j * 32);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const float2 t = cs[i];
-              const float a = __uint_as_float(x0[i]);
-              const float b = __uint_as_float(x1[i]);
-              o0[i] = a * t.x - b * t.y;
-              o1[i] = b * t.x + a * t.y;
+            for (int i = 0; i < 32; i += 2) {
+              const float4 t = __ldg(cs + i / 2);
+              const float a0 = __uint_as_float(x0[i]), b0 = __uint_as_float(x1[i]);
+              const float a1 = __uint_as_float(x0[i + 1]), b1 = __uint_as_float(x1[i + 1]);
+              o0[i] = a0 * t.x - b0 * t.y;
+              o1[i] = b0 * t.x + a0 * t.y;
+              o0[i + 1] = a1 * t.z - b1 * t.w;
+              o1[i + 1] = b1 * t.z + a1 * t.w;
             }
           } else {
 #pragma unroll
