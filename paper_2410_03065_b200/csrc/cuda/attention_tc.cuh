@@ -17,11 +17,12 @@
 // more than 2^8, so the common block costs no O round trip.
 // Q lives in TMEM (the A operand of QK^T, like P for PV), so each block's
 // MMAs read only K and V from shared memory.
-// Roles (384 threads): warp 0 TMA producer of K (3-stage ring, freed
+// Roles (128 + 128*NG threads): warp 0 TMA producer of K (3-stage ring, freed
 // right after each QK^T), warp 2 TMA producer of V (2-stage ring, freed after
-// each PV), warp 1 TMEM owner + MMA issuer, warps 4-11 softmax + epilogue in
-// two column groups (warp w%4 owns TMEM lanes 32*(w%4)..; two warps per
-// sub-partition hide the MUFU / TMEM-load latency of the row chains).
+// each PV), warp 1 TMEM owner + MMA issuer, warps 4.. softmax + epilogue in
+// NG column groups (warp w%4 owns TMEM lanes 32*(w%4)..; NG = 2: two softmax
+// warps per sub-partition hide the MUFU / TMEM-load latency of the row chains;
+// NG = 4 measured 10% slower at 32K).
 #pragma once
 
 #include "attention.cuh"
@@ -31,7 +32,9 @@ namespace cake_dev {
 
 constexpr int kFaRows = 128;
 constexpr int kFaKeys = 128;  // two pages
-constexpr int kFaThreads = 384;  // 4 role warps + 2 softmax groups of 4 warps
+// 4 role warps + NG softmax groups of 4 warps
+template <int NG>
+constexpr int fa_threads() { return 128 + NG * 128; }
 
 template <int HD>
 struct FaCfg {
@@ -96,11 +99,9 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-// pairs i of the 32 per half-block row whose exponentials go to ex2_poly
-constexpr unsigned kFaPolyPairs = 0x88888888u;  // every 4th pair: 25%
 
-template <int HD>
-__global__ void __launch_bounds__(kFaThreads, 1)
+template <int HD, int NG>
+__global__ void __launch_bounds__(fa_threads<NG>(), 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
                    const FaArgs a) {
   using Cfg = FaCfg<HD>;
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_kv);
-    mbar_init(q_ready, 256);
+    mbar_init(q_ready, 128 * NG);
     for (int s = 0; s < Cfg::kKStages; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_ready[s], 256);
+      mbar_init(&p_ready[s], 128 * NG);
     }
     mbar_init(pv_done, 1);
     mbar_init(o_final, 1);
@@ -263,13 +264,18 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ softmax + epilogue
-    // Two groups of 4 warps share the TMEM lanes (rows): group g owns score
-    // columns [64g, 64g+64), P columns [32g, 32g+32) and O columns
-    // [g*HD/2, (g+1)*HD/2). The row max is exchanged through shared memory
-    // once per block (double-buffered by block parity), the row sum once at
-    // the end, so both groups take identical rescale decisions.
-    __shared__ float xmax[2][2][kFaRows];
-    __shared__ float xsum[2][kFaRows];
+    // NG groups of 4 warps share the TMEM lanes (rows): group g owns score
+    // columns [g*128/NG, (g+1)*128/NG), the matching packed P columns and O
+    // columns [g*HD/NG, (g+1)*HD/NG). More groups = more warps per SM
+    // sub-partition to hide the TMEM-load / MUFU latency of the row chains.
+    // The row max is exchanged through shared memory once per block
+    // (double-buffered by block parity), the row sum once at the end, so all
+    // groups take identical rescale decisions.
+    constexpr int kKeysPerG = kFaKeys / NG;
+    constexpr int kOCols = HD / NG;
+    constexpr int kQWords = HD / 2 / NG;  // packed bf16 pairs of Q per group
+    __shared__ float xmax[2][NG][kFaRows];
+    __shared__ float xsum[NG][kFaRows];
     const int g = (warp - 4) >> 2;
     const int q4 = warp & 3;
     const int row = q4 * 32 + static_cast<int>(lane);
@@ -279,27 +285,26 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     const long long kmax_valid = static_cast<long long>(p_end) * kAttnPage;  // keys past the split are absent
     const long long qpos_min = a.chunk_start + tok0;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
-    constexpr int kHalfKeys = kFaKeys / 2;
-    constexpr int kOCols = HD / 2;
     const float sc = a.scale_log2;
     {
-      // this thread's Q row, half g (HD/2 bf16 = HD/4 packed columns), into TMEM
+      // this thread's Q row, slice g (HD/NG bf16 = kQWords packed columns), into TMEM
       uint32_t qv[32];
       const bool live = t < a.chunk_len && nb > 0;
       const uint4* src = reinterpret_cast<const uint4*>(a.q + (static_cast<size_t>(t) * a.n_q_heads + head) * HD +
-                                                        g * (HD / 2));
+                                                        g * (HD / NG));
 #pragma unroll
-      for (int i = 0; i < HD / 16; ++i) {
+      for (int i = 0; i < kQWords / 4; ++i) {
         const uint4 v = live ? __ldg(src + i) : make_uint4(0u, 0u, 0u, 0u);
         qv[4 * i] = v.x;
         qv[4 * i + 1] = v.y;
         qv[4 * i + 2] = v.z;
         qv[4 * i + 3] = v.w;
       }
-      if constexpr (HD == 128) {
-        tmem_st32(tmem + lane_off + Cfg::kColQ + g * 32, qv);
+      if constexpr (kQWords == 32) {
+        tmem_st32(tmem + lane_off + Cfg::kColQ + g * kQWords, qv);
       } else {
-        tmem_st16(tmem + lane_off + Cfg::kColQ + g * 16, qv);
+        static_assert(kQWords == 16, "Q slice per group");
+        tmem_st16(tmem + lane_off + Cfg::kColQ + g * kQWords, qv);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -311,29 +316,31 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       mbar_wait(&s_full[s], (j >> 1) & 1);
       tc_fence_after();
       const uint32_t tS = tmem + lane_off + (s ? Cfg::kColS1 : Cfg::kColS0);
-      float sv[kHalfKeys];
+      float sv[kKeysPerG];
 #pragma unroll
-      for (int c = 0; c < kHalfKeys / 32; ++c) {
+      for (int c = 0; c < kKeysPerG / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(tS + g * kHalfKeys + c * 32, r);
+        tmem_ld32(tS + g * kKeysPerG + c * 32, r);
         tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; ++i) sv[c * 32 + i] = __uint_as_float(r[i]);
       }
-      const long long kbase = static_cast<long long>(p_begin + 2 * j) * kAttnPage + g * kHalfKeys;
-      if (kbase + kHalfKeys - 1 > qpos_min || kbase + kHalfKeys > kmax_valid) {
+      const long long kbase = static_cast<long long>(p_begin + 2 * j) * kAttnPage + g * kKeysPerG;
+      if (kbase + kKeysPerG - 1 > qpos_min || kbase + kKeysPerG > kmax_valid) {
 #pragma unroll
-        for (int i = 0; i < kHalfKeys; ++i) {
+        for (int i = 0; i < kKeysPerG; ++i) {
           const long long key = kbase + i;
           if (key > qpos || key >= kmax_valid) sv[i] = -INFINITY;
         }
       }
       float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < kHalfKeys; ++i) mx = fmaxf(mx, sv[i]);
+      for (int i = 0; i < kKeysPerG; ++i) mx = fmaxf(mx, sv[i]);
       xmax[s][g][row] = mx;
-      named_bar_sync(2, 256);
-      mx = fmaxf(xmax[s][0][row], xmax[s][1][row]) * sc;  // scale > 0: max commutes
+      named_bar_sync(2, 128 * NG);
+#pragma unroll
+      for (int h = 0; h < NG; ++h) mx = fmaxf(mx, xmax[s][h][row]);
+      mx *= sc;  // scale > 0: max commutes
       if (mx > m + 8.0f) {  // (also true on the first block with a visible key)
         if (m != -INFINITY) {
           // move the reference max: O (blocks < j, i.e. after PV(j-1)) and l scale by 2^(m - mx)
@@ -360,11 +367,10 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       uint32_t pk[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const bool poly = (kFaPolyPairs >> i) & 1u;
+      for (int i = 0; i < kKeysPerG / 2; ++i) {
         const float2 x = ffma2(make_float2(sv[2 * i], sv[2 * i + 1]), sc2, nb2);
         float2 p;
-        if (poly) {
+        if ((i & 3) == 3) {  // every 4th pair on the FMA pipe: 25% of the exponentials off MUFU
           p = ex2_poly2(x);
         } else {
           p.x = ex2_approx(x.x);
@@ -373,17 +379,22 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         rs[i & 3] = fadd2(rs[i & 3], p);
         pk[i] = pack_bf16(p.x, p.y);
       }
-      tmem_st32(tS + g * 32, pk);
+      if constexpr (kKeysPerG / 2 == 32)
+        tmem_st32(tS + g * 32, pk);
+      else
+        tmem_st16(tS + g * 16, pk);
       const float2 rs01 = fadd2(rs[0], rs[1]), rs23 = fadd2(rs[2], rs[3]);
       l += (rs01.x + rs23.x) + (rs01.y + rs23.y);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_ready[s]);
     }
-    // epilogue: total row sum, then this group's half of O
+    // epilogue: total row sum, then this group's slice of O
     xsum[g][row] = l;
-    named_bar_sync(2, 256);
-    l = xsum[0][row] + xsum[1][row];
+    named_bar_sync(2, 128 * NG);
+    l = 0.f;
+#pragma unroll
+    for (int h = 0; h < NG; ++h) l += xsum[h][row];
     const bool valid = t < a.chunk_len;
     const size_t orow = static_cast<size_t>(t) * a.n_q_heads + head;
     const float inv = l > 0.f ? 1.f / l : 0.f;
