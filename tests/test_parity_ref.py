@@ -109,3 +109,26 @@ def test_live_modeled_run_same_split(tmp_path, cake_b200, cake_ref):
                        throttle_quantum_bytes=64 << 10)
         assert sorted(c.index for c in live.chunks) == list(range(8))
         assert abs(live.merge_point - sim.merge_point) <= 1
+
+
+def test_cached_prefix_plan(tmp_path, cake_b200):
+    """B200 extension (RunOptions::cached_prefix): a store holding only the first
+    chunks of the prompt. Without the option the run fails like the reference
+    (MissingKeyError for the first absent chunk); with it the plan splits into the
+    cached prefix and an uncached suffix, which only a GPU live run can compute;
+    on a fully cached prompt the option changes nothing."""
+    s = cake_b200.store(str(tmp_path / "part"), create=1)
+    s.populate(1024, 256, (2, 256, 2), "identity", seed=42)  # chunks 0..3 of an 8-chunk prompt
+    cost = CostModel(12.0, 0.02, 256)
+    tr = BandwidthTrace.constant(400)
+    with pytest.raises(MissingKeyError):
+        cake_b200.run(s, 2048, 256, (2, 256, 2), "identity", cost, tr, "cake", "sim", 42)
+    with pytest.raises(ValueError, match="GPU live run"):
+        cake_b200.run(s, 2048, 256, (2, 256, 2), "identity", cost, tr, "cake", "sim", 42, cached_prefix=True)
+    full = cake_b200.run(s, 1024, 256, (2, 256, 2), "identity", cost, tr, "cake", "sim", 42)
+    opt = cake_b200.run(s, 1024, 256, (2, 256, 2), "identity", cost, tr, "cake", "sim", 42, cached_prefix=True)
+    assert (full.ttft_us, full.merge_point) == (opt.ttft_us, opt.merge_point)
+    # a prompt whose first chunk is absent has no cached prefix at all
+    empty = cake_b200.store(str(tmp_path / "none"), create=1)
+    with pytest.raises(MissingKeyError):
+        cake_b200.run(empty, 1024, 256, (2, 256, 2), "identity", cost, tr, "cake", "sim", 42, cached_prefix=True)
