@@ -183,6 +183,8 @@ CAKE_API int cake_gpu_read_chunk(const cake_gpu* g, uint64_t token_start, uint32
 CAKE_API int cake_gpu_kernel_stats(cake_gpu* g, cake_kernel_stat* out, int reset);
 /* Event-bracket kernel classes (bit CAKE_K_*; -1 all, 0 none) from now on. */
 CAKE_API int cake_gpu_set_profiling(cake_gpu* g, int mask);
+/* Bracket only every n-th launch of a profiled class (n >= 1). */
+CAKE_API int cake_gpu_set_profiling_stride(cake_gpu* g, int stride);
 /* 0 = tcgen05 attention (default), 1 = mma.sync attention (validation cross-check). */
 CAKE_API int cake_gpu_set_attention_impl(cake_gpu* g, int impl);
 CAKE_API void* cake_gpu_model(cake_gpu* g); /* cake_model* for direct C-ABI CUDA calls */

@@ -204,6 +204,8 @@ typedef struct cake_kernel_stat {
 /* mask bit k (CAKE_K_*): every launch of kernel class k is bracketed by CUDA
  * events on its stream (-1 = all, 0 = off); stats resolve (and reset) on read. */
 CAKE_API int cake_model_set_profiling(cake_model* m, int mask);
+/* Bracket only every n-th launch of a profiled class (n >= 1; default 1). */
+CAKE_API int cake_model_set_profiling_stride(cake_model* m, int stride);
 CAKE_API int cake_model_kernel_stats(cake_model* m, cake_kernel_stat* out /* [CAKE_K_COUNT] */, int reset);
 CAKE_API int cake_model_launch_count(cake_model* m, long long* n, int reset);
 

@@ -425,6 +425,8 @@ struct cake_model {
   ncclComm_t comm = nullptr;
   bool emulated_tp = false;  // test driver sums the ranks' partials itself (cake_prefill_group)
   unsigned profile_mask = 0;  // bit k: bracket launches of kernel class k with events
+  int profile_stride = 1;     // bracket every n-th launch of a class (keeps the other PDL chains intact)
+  long long prof_seq[CAKE_K_COUNT]{};
   std::mutex prof_mu;  // launches come from the compute thread and the loader's pacer thread
   std::vector<ProfPair> prof;
   std::vector<cudaEvent_t> event_pool;
@@ -456,7 +458,7 @@ struct ProfScope {
       : m(m_), kind(kind_), s(s_), flops(f), bytes(b) {
     std::lock_guard<std::mutex> g(m->prof_mu);
     m->launches++;
-    if (m->profile_mask & (1u << kind)) {
+    if ((m->profile_mask & (1u << kind)) && m->prof_seq[kind]++ % m->profile_stride == 0) {
       a = pool_event(m);
       cudaEventRecord(a, s);
     }
@@ -1304,6 +1306,13 @@ int cake_model_set_comm(cake_model* m, void* comm) {
 int cake_model_set_profiling(cake_model* m, int mask) {
   std::lock_guard<std::mutex> g(m->prof_mu);
   m->profile_mask = static_cast<unsigned>(mask);
+  return CAKE_OK;
+}
+
+int cake_model_set_profiling_stride(cake_model* m, int stride) {
+  if (stride < 1) return fail(CAKE_EINVAL, "profiling stride must be >= 1");
+  std::lock_guard<std::mutex> g(m->prof_mu);
+  m->profile_stride = stride;
   return CAKE_OK;
 }
 

@@ -489,6 +489,13 @@ int cake_gpu_set_profiling(cake_gpu* g, int mask) {
   });
 }
 
+int cake_gpu_set_profiling_stride(cake_gpu* g, int stride) {
+  return guarded([&] {
+    if (cake_model_set_profiling_stride(g->ctx->model(), stride) != CAKE_OK)
+      throw std::invalid_argument("profiling stride must be >= 1");
+  });
+}
+
 int cake_gpu_set_attention_impl(cake_gpu* g, int impl) {
   return guarded([&] {
     if (cake_model_set_attention_impl(g->ctx->model(), impl) != CAKE_OK) throw std::invalid_argument("bad impl");

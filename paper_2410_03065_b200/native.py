@@ -104,6 +104,7 @@ _SIGS = {
     "cake_gpu_read_chunk": (C.c_int, [vp, u64, u32, vp, u64]),
     "cake_gpu_kernel_stats": (C.c_int, [vp, P(CakeKernelStat), C.c_int]),
     "cake_gpu_set_profiling": (C.c_int, [vp, C.c_int]),
+    "cake_gpu_set_profiling_stride": (C.c_int, [vp, C.c_int]),
     "cake_gpu_set_attention_impl": (C.c_int, [vp, C.c_int]),
     "cake_gpu_model": (vp, [vp]),
     "cake_gpu_compute_stream": (vp, [vp]),

@@ -139,8 +139,10 @@ class GpuRuntime:
         self.n.call("cake_gpu_set_attention_impl", self.h,
                     {"tcgen05": 0, "mma_sync": 1, "tcgen05_1tile": 2, "tcgen05_2tile": 3}[impl])
 
-    def set_profiling(self, kernels="all"):
-        """Bracket launches of the named kernel classes with CUDA events ("all", None, or a list)."""
+    def set_profiling(self, kernels="all", stride: int = 1):
+        """Bracket launches of the named kernel classes with CUDA events ("all", None, or a list);
+        stride n brackets every n-th launch of a class only."""
+        self.n.call("cake_gpu_set_profiling_stride", self.h, stride)
         if kernels == "all":
             mask = -1
         elif not kernels:
