@@ -720,7 +720,9 @@ int launch_skinny(cake_model* m, int kind, const SkinnyArgs& a, double rows, cud
     cfgd = true;
   }
   const int smem = a.M * a.K * 2;
-  const int blocks = std::max(1, std::min((a.units + kSkinnyWarps - 1) / kSkinnyWarps, num_sms() * 16));
+  // 4 CTAs per SM, warps striding over the units: the per-CTA prologue (x into smem,
+  // or its RMSNorm) is paid 4x per SM instead of once per 8 units
+  const int blocks = std::max(1, std::min((a.units + kSkinnyWarps - 1) / kSkinnyWarps, num_sms() * 4));
   ProfScope ps(m, kind, s, 2.0 * a.M * rows * a.K, 2.0 * rows * a.K);
   CK(launch_chain(kern, dim3(blocks), dim3(kSkinnyWarps * 32), smem, s, 1, a));
   CKL();
@@ -767,11 +769,13 @@ int last_token_pass(cake_model* m, const int32_t* d_token, long long T, const in
   }
   for (int l = 0; l < m->L; ++l) {
     LayerWeights& lw = m->layers[l];
-    CKS(rmsnorm(m, lw.ln1, 0, 1, nullptr, s));
     {
       SkinnyArgs a{};
       a.W = lw.wqkv;  // q rows come first
       a.x = m->xn;
+      a.norm_h = m->h;  // ln1 folded into the projection (skinny.cuh)
+      a.norm_gamma = lw.ln1;
+      a.norm_eps = m->cfg.rms_eps;
       a.M = 1;
       a.K = H;
       a.units = m->nq * m->hd / 2;
@@ -784,11 +788,13 @@ int last_token_pass(cake_model* m, const int32_t* d_token, long long T, const in
     }
     CKS(attention(m, T - 1, 1, l, bt, nullptr, s));
     CKS(skinny_row_parallel(m, CAKE_K_GEMM_O, lw.wo, m->attn, m->nq * m->hd, s));
-    CKS(rmsnorm(m, lw.ln2, 0, 1, nullptr, s));
     {
       SkinnyArgs a{};
       a.W = lw.wgu;
       a.x = m->xn;
+      a.norm_h = m->h;  // ln2 folded in
+      a.norm_gamma = lw.ln2;
+      a.norm_eps = m->cfg.rms_eps;
       a.M = 1;
       a.K = H;
       a.units = m->F;
