@@ -100,6 +100,8 @@ typedef struct cake_store cake_store;
 /* root == NULL or "": memory-resident store (pinned when pinned != 0). create: 0 open, 1 create, 2 open_or_create */
 CAKE_API int cake_store_open(const char* root, int create, int pinned, cake_store** out);
 CAKE_API int cake_store_close(cake_store* s);
+/* B200 extension: file-backed stores read aligned slices with O_DIRECT (page-cache bypass). */
+CAKE_API int cake_store_set_direct_io(cake_store* s, int on);
 CAKE_API int cake_store_entry_count(const cake_store* s, uint64_t* n);
 /* populate(store, request, profile, codec, seed, kind) — reference proj/src/store.cpp:303-334 */
 CAKE_API int cake_store_populate(cake_store* s, uint64_t total_tokens, uint32_t chunk_size, uint32_t n_layers,

@@ -229,6 +229,10 @@ class ChunkStore:
             self.n.lib.cake_store_close(self.h)
             self.h = None
 
+    def set_direct_io(self, on: bool = True):
+        """File-backed stores: read aligned slices with O_DIRECT (B200 extension)."""
+        self.n.call("cake_store_set_direct_io", self.h, 1 if on else 0)
+
     def __del__(self):
         try:
             self.close()

@@ -249,6 +249,16 @@ int cake_store_close(cake_store* s) {
   return 0;
 }
 
+int cake_store_set_direct_io(cake_store* s, int on) {
+  return guarded([&] {
+#ifndef CAKE_REFERENCE_BUILD
+    s->store.set_direct_io(on != 0);
+#else
+    if (on) throw std::invalid_argument("direct I/O is a B200 extension");
+#endif
+  });
+}
+
 int cake_store_entry_count(const cake_store* s, uint64_t* n) {
   return guarded([&] { *n = s->store.entry_count(); });
 }

@@ -7,7 +7,9 @@
 #include <condition_variable>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <unordered_map>
 #include <stdexcept>
 #include <thread>
 
@@ -31,6 +33,41 @@ void* pinned_alloc(std::size_t n, void*) {
   return cake_host_alloc(&p, n) == CAKE_OK ? p : nullptr;
 }
 void pinned_release(void* p, void*) { cake_host_free(p); }
+
+// Landing buffers of file-backed tiers: pinned memory kept across chunks and
+// runs (a cudaHostAlloc of a 64-MiB chunk costs milliseconds; a run holds
+// only the chunk the reader fills and the ones the pacer is still copying).
+struct PinnedPool {
+  std::mutex mu;
+  std::multimap<std::size_t, void*> free_;  // size -> buffer
+  std::unordered_map<void*, std::size_t> size_of;
+  ~PinnedPool() {
+    for (auto& kv : free_) cake_host_free(kv.second);
+  }
+  static void* alloc(std::size_t n, void* ctx) {
+    auto* pool = static_cast<PinnedPool*>(ctx);
+    {
+      std::lock_guard g(pool->mu);
+      auto it = pool->free_.lower_bound(n);
+      if (it != pool->free_.end() && it->first <= 2 * n) {
+        void* p = it->second;
+        pool->free_.erase(it);
+        return p;
+      }
+    }
+    void* p = pinned_alloc(n, nullptr);
+    if (p) {
+      std::lock_guard g(pool->mu);
+      pool->size_of[p] = n;
+    }
+    return p;
+  }
+  static void release(void* p, void* ctx) {
+    auto* pool = static_cast<PinnedPool*>(ctx);
+    std::lock_guard g(pool->mu);
+    pool->free_.emplace(pool->size_of.at(p), p);
+  }
+};
 
 struct Event {
   void* h = nullptr;
@@ -120,6 +157,7 @@ struct GpuContext::Impl {
   GpuRunInfo last;
   std::unique_ptr<TpCoordinator> tp;
   std::uint64_t run_counter = 0;
+  PinnedPool landing;  // file-tier landing buffers, reused across runs
 
   void ensure_events(std::size_t n) {
     for (auto* v : {&ev_start, &ev_near, &ev_end, &ev_io})
@@ -560,7 +598,7 @@ class GpuLoaderSink final : public ChunkSink {
 
   bool keep_going(const FetchTask& t) override { return r_.commit[t.chunk.index].load() != kByCompute; }
 
-  HostAllocator staging_allocator() override { return {pinned_alloc, pinned_release, nullptr}; }
+  HostAllocator staging_allocator() override { return {PinnedPool::alloc, PinnedPool::release, &r_.g.landing}; }
 
   std::uint64_t h2d_bytes() const { return h2d_bytes_; }
 

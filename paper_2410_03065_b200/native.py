@@ -77,6 +77,7 @@ _SIGS = {
                                P(CakeRunOpts), P(CakeSummary), P(CakeRecord)]),
     "cake_store_open": (C.c_int, [C.c_char_p, C.c_int, C.c_int, P(vp)]),
     "cake_store_close": (C.c_int, [vp]),
+    "cake_store_set_direct_io": (C.c_int, [vp, C.c_int]),
     "cake_store_entry_count": (C.c_int, [vp, P(u64)]),
     "cake_store_populate": (C.c_int, [vp, u64, u32, u32, u32, u32, C.c_char_p, u64, C.c_int, vp]),
     "cake_store_put": (C.c_int, [vp, vp, vp, u64, u32, C.c_char_p, u64]),

@@ -168,3 +168,25 @@ def test_partially_cached_prompt(setup, mode):
     assert np.array_equal(rt.logits(), want)
     with pytest.raises(Exception):
         rt.run(part, T, C, 42, mbps=1000, mode=mode)  # without the option a missing chunk is an error
+
+
+@pytest.mark.parametrize("direct", [False, True])
+def test_file_tier(setup, tmp_path, direct):
+    """Cache tier on local disk in the reference's file format (one file per
+    chunk + manifest), read by the loader with buffered or O_DIRECT reads:
+    the assembled cache and the logits equal the pinned-memory tier's."""
+    from paper_2410_03065_b200.cake import ChunkStore
+
+    rt, T, C = setup["rt"], setup["T"], setup["C"]
+    rt.run(setup["tier"], T, C, 42, mbps=8000, mode="io_only")
+    want_kv = [rt.read_chunk(s, C) for s in range(0, T, C)]
+    want = rt.logits()
+    fs = ChunkStore(rt.n, str(tmp_path / f"tier{int(direct)}"), create=1)
+    rt.build_cache_tier(T, C, 42, store=fs)
+    fs.set_direct_io(direct)
+    for mode in ("io_only", "cake"):
+        r = rt.run(fs, T, C, 42, mbps=8000, mode=mode)
+        assert sorted(c.index for c in r.chunks) == list(range(T // C))
+        assert [rt.read_chunk(s, C) for s in range(0, T, C)] == want_kv
+        assert np.array_equal(rt.logits(), want)
+    fs.close()
