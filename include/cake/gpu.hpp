@@ -69,6 +69,9 @@ struct GpuOptions {
   CostModel prior{5.0, 0.0002, 512};  // per-chunk duration prior (refine with calibrate())
   Micros race_margin_us = 200;        // race only when predicted to win by at least this
   bool profile_kernels = false;       // bracket tracked kernels with events (bench roofline)
+  // GPU share of the compute side: > 0 confines the
+  // compute stream to this many SMs (green context); 0 = the whole GPU.
+  int compute_sms = 0;
 };
 
 struct GpuRunInfo {

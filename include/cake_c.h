@@ -146,6 +146,7 @@ typedef struct cake_gpu_config {
   int profile_kernels;
   int64_t race_margin_us;
   const char* tp_shm; /* POSIX shm name of the TP group's coordinator (tp_size > 1), NULL otherwise */
+  int compute_sms;    /* > 0: confine the compute stream to this many SMs (GPU-share emulation) */
 } cake_gpu_config;
 
 typedef struct cake_gpu_result {

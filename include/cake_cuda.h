@@ -60,6 +60,12 @@ CAKE_API int cake_cuda_device_sync(void);
 /* ---------------------------------------------------------- streams/events */
 CAKE_API int cake_stream_create(void** stream, int high_priority);
 CAKE_API int cake_stream_destroy(void* stream);
+/* A stream confined to (at least) n_sms SMs (green context over an SM
+ * partition); n_sms <= 0 or >= the device's count gives a normal stream.
+ * got_sms receives the partition size. GPU-share emulation. */
+CAKE_API int cake_stream_create_sm_share(void** stream, int n_sms, int* got_sms);
+/* Launch sizing (persistent grids, split counts) for an SM budget; 0 = the device. */
+CAKE_API int cake_set_sm_budget(int n_sms);
 CAKE_API int cake_stream_sync(void* stream);
 CAKE_API int cake_stream_wait_event(void* stream, void* event);
 CAKE_API int cake_event_create(void** event, int timing);

@@ -152,6 +152,7 @@ int make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint
 }
 
 int g_num_sms = 0;
+int g_sm_limit = 0;  // > 0: the compute stream owns this many SMs (green context); launches size to it
 int num_sms() {
   if (g_num_sms == 0) {
     int dev = 0;
@@ -159,7 +160,7 @@ int num_sms() {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
-  return g_num_sms;
+  return g_sm_limit > 0 ? std::min(g_sm_limit, g_num_sms) : g_num_sms;
 }
 
 // Stream-K scratch shared by every GEMM launch of the process (launches are
@@ -206,6 +207,11 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaSt
   auto kern = gemm_tc_kernel<BN, EPI>;
   static bool configured = false;
   static int max_clusters[3] = {0, 0, 0};
+  static int clusters_for_sms = 0;  // the SM budget max_clusters was computed for
+  if (clusters_for_sms != num_sms()) {
+    max_clusters[0] = max_clusters[1] = max_clusters[2] = 0;
+    clusters_for_sms = num_sms();
+  }
   if (!configured) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
     configured = true;
@@ -255,6 +261,7 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
   auto kern = gemm2_tc_kernel<BLOCK_N, EPI>;
   static bool configured = false;
   static int max_pairs = 0;
+  static int pairs_for_sms = 0;  // the SM budget max_pairs was computed for
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -268,6 +275,9 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
   cfg.numAttrs = 1;
   if (!configured) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+    configured = true;
+  }
+  if (pairs_for_sms != num_sms()) {
     cfg.gridDim = dim3(32);
     int n = 0;
     if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
@@ -275,8 +285,8 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
       n = num_sms() / 2;
     }
     max_pairs = std::min(n, num_sms() / 2);
+    pairs_for_sms = num_sms();
     if (std::getenv("CAKE_DEBUG_GEMM")) std::fprintf(stderr, "gemm2: occupancy reports %d co-resident pairs\n", n);
-    configured = true;
   }
   a.num_m_blocks = (a.M + kGemmBlockM - 1) / kGemmBlockM;
   a.num_n_blocks = a.N / BLOCK_N;
@@ -984,6 +994,61 @@ int cake_stream_create(void** stream, int high_priority) {
   *stream = s;
   return CAKE_OK;
 }
+// A stream whose kernels run on (at least) n_sms SMs only: a green context
+// over an SM partition of the device. SURVEY §8(f) item 4 / PAPER.md:331:
+// the reference scales its modeled chunk latency by a GPU-share factor p; on
+// the B200 the compute side gets a real fraction of the SMs instead.
+int cake_stream_create_sm_share(void** stream, int n_sms, int* got_sms) {
+  using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+  using Split = CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned);
+  using GenDesc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned);
+  using GreenCreate = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
+  using GreenStream = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
+  auto entry = [](const char* name) -> void* {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return p;
+  };
+  auto get_res = reinterpret_cast<GetRes>(entry("cuDeviceGetDevResource"));
+  auto split = reinterpret_cast<Split>(entry("cuDevSmResourceSplitByCount"));
+  auto gen = reinterpret_cast<GenDesc>(entry("cuDevResourceGenerateDesc"));
+  auto gcreate = reinterpret_cast<GreenCreate>(entry("cuGreenCtxCreate"));
+  auto gstream = reinterpret_cast<GreenStream>(entry("cuGreenCtxStreamCreate"));
+  if (!get_res || !split || !gen || !gcreate || !gstream) return fail(CAKE_ESTATE, "green contexts unavailable");
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaFree(nullptr));  // the primary context exists
+  CUdevResource all{}, group{}, rest{};
+  if (get_res(static_cast<CUdevice>(dev), &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
+    return fail(CAKE_ECUDA, "cuDeviceGetDevResource failed");
+  if (n_sms <= 0 || static_cast<unsigned>(n_sms) >= all.sm.smCount) {
+    CKS(cake_stream_create(stream, 0));
+    if (got_sms) *got_sms = static_cast<int>(all.sm.smCount);
+    return CAKE_OK;
+  }
+  unsigned nb = 1;
+  if (split(&group, &nb, &all, &rest, 0, static_cast<unsigned>(n_sms)) != CUDA_SUCCESS || nb != 1)
+    return fail(CAKE_ECUDA, "cuDevSmResourceSplitByCount(%d) failed", n_sms);
+  CUdevResourceDesc desc;
+  if (gen(&desc, &group, 1) != CUDA_SUCCESS) return fail(CAKE_ECUDA, "cuDevResourceGenerateDesc failed");
+  CUgreenCtx gctx;
+  if (gcreate(&gctx, desc, static_cast<CUdevice>(dev), CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+    return fail(CAKE_ECUDA, "cuGreenCtxCreate failed");
+  CUstream st;
+  if (gstream(&st, gctx, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
+    return fail(CAKE_ECUDA, "cuGreenCtxStreamCreate failed");
+  *stream = st;  // (the green context lives as long as the process)
+  if (got_sms) *got_sms = static_cast<int>(group.sm.smCount);
+  return CAKE_OK;
+}
+
+int cake_set_sm_budget(int n_sms) {
+  g_sm_limit = std::max(0, n_sms);
+  return CAKE_OK;
+}
+
 int cake_stream_destroy(void* stream) {
   CK(cudaStreamDestroy(S(stream)));
   return CAKE_OK;

@@ -394,6 +394,7 @@ int cake_gpu_create(const cake_gpu_config* c, cake_gpu** out) {
     o.profile_kernels = c->profile_kernels != 0;
     if (c->race_margin_us > 0) o.race_margin_us = c->race_margin_us;
     if (c->tp_shm) o.tp_shm = c->tp_shm;
+    o.compute_sms = c->compute_sms;
     auto g = std::make_unique<cake_gpu>();
     g->ctx = std::make_unique<GpuContext>(m, o);
     *out = g.release();

@@ -158,6 +158,7 @@ struct GpuContext::Impl {
   std::unique_ptr<TpCoordinator> tp;
   std::uint64_t run_counter = 0;
   PinnedPool landing;  // file-tier landing buffers, reused across runs
+  int compute_sms = 0;  // > 0: the compute stream's SM partition
 
   void ensure_events(std::size_t n) {
     for (auto* v : {&ev_start, &ev_near, &ev_end, &ev_io})
@@ -205,7 +206,15 @@ GpuContext::GpuContext(const GpuModelConfig& cfg, const GpuOptions& opt) : impl_
   if (opt.tp_size > 1 && !opt.tp_shm.empty())
     g.tp = std::make_unique<TpCoordinator>(opt.tp_shm, opt.tp_rank, opt.tp_size);
   check(cake_model_set_profiling(g.model, opt.profile_kernels ? -1 : 0), "profiling");
-  check(cake_stream_create(&g.s_compute, 0), "stream");
+  if (opt.compute_sms > 0) {
+    int got = 0;
+    check(cake_stream_create_sm_share(&g.s_compute, opt.compute_sms, &got), "compute stream (SM share)");
+    check(cake_set_sm_budget(got), "sm budget");
+    g.compute_sms = got;
+  } else {
+    check(cake_set_sm_budget(0), "sm budget");
+    check(cake_stream_create(&g.s_compute, 0), "stream");
+  }
   check(cake_stream_create(&g.s_copy, 1), "stream");     // loader work jumps the queue for free SMs
   check(cake_stream_create(&g.s_control, 1), "stream");
   g.n_pages = g.info.n_logical_pages;
@@ -235,6 +244,7 @@ GpuContext::~GpuContext() {
   for (void* s : {g.s_compute, g.s_copy, g.s_control})
     if (s) cake_stream_destroy(s);
   if (g.model) cake_model_destroy(g.model);
+  if (g.compute_sms > 0) cake_set_sm_budget(0);  // later contexts size launches for the whole device
 }
 
 cake_model* GpuContext::model() const { return impl_->model; }

@@ -46,7 +46,7 @@ class CakeGpuConfig(C.Structure):
                 ("rms_eps", C.c_float), ("max_chunk", C.c_int), ("max_tokens", C.c_longlong),
                 ("weight_seed", C.c_ulonglong), ("device", C.c_int), ("tp_rank", C.c_int), ("tp_size", C.c_int),
                 ("nccl_comm", vp), ("lookahead_layers", C.c_int), ("profile_kernels", C.c_int),
-                ("race_margin_us", i64), ("tp_shm", C.c_char_p)]
+                ("race_margin_us", i64), ("tp_shm", C.c_char_p), ("compute_sms", C.c_int)]
 
 
 class CakeGpuResult(C.Structure):

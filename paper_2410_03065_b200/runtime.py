@@ -50,7 +50,8 @@ class GpuRuntime:
     def __init__(self, preset, *, n_layers: int | None = None, max_chunk: int = 512, max_tokens: int = 32768,
                  weight_seed: int = 1234, device: int = 0, tp_rank: int = 0, tp_size: int = 1, nccl_comm=None,
                  lookahead_layers: int = 0, profile_kernels: bool = False, race_margin_us: int = 0,
-                 rope_theta: float = 500000.0, rms_eps: float = 1e-5, tp_shm: str | None = None):
+                 rope_theta: float = 500000.0, rms_eps: float = 1e-5, tp_shm: str | None = None,
+                 compute_sms: int = 0):
         self.n = N.load()
         dims = PRESETS[preset] if isinstance(preset, str) else tuple(preset)
         L, H, nh, nkv, hd, ffn, vocab = dims
@@ -60,7 +61,7 @@ class GpuRuntime:
         cfg = N.CakeGpuConfig(L, H, nh, nkv, hd, ffn, vocab, rope_theta, rms_eps, max_chunk, max_tokens,
                               weight_seed, device, tp_rank, tp_size, nccl_comm, lookahead_layers,
                               1 if profile_kernels else 0, race_margin_us,
-                              tp_shm.encode() if tp_shm else None)
+                              tp_shm.encode() if tp_shm else None, compute_sms)
         h = N.vp()
         self.n.call("cake_gpu_create", C.byref(cfg), C.byref(h))
         self.h = h.value

@@ -190,3 +190,32 @@ def test_file_tier(setup, tmp_path, direct):
         assert [rt.read_chunk(s, C) for s in range(0, T, C)] == want_kv
         assert np.array_equal(rt.logits(), want)
     fs.close()
+
+
+def test_sm_share_compute_stream(setup):
+    """GPU-share emulation: a runtime whose compute stream owns a fraction of
+    the SMs (green context). Launches are sized for the partition (split
+    counts, persistent grids), so its sums run in another order than the
+    full-GPU runtime's: within tolerance of it, and bit-identical to itself
+    wherever the merge point lands."""
+    from paper_2410_03065_b200.runtime import GpuRuntime
+
+    rt, T, C = setup["rt"], setup["T"], setup["C"]
+    rt.run(setup["tier"], T, C, 42, mbps=1000, mode="compute_only")
+    full_kv = [_chunk_kv(rt, s, C) for s in range(0, T, C)]
+    full = rt.logits()
+    small = GpuRuntime(setup["dims"], max_tokens=T, max_chunk=C, compute_sms=16)
+    try:
+        tier = small.build_cache_tier(T, C, 42)
+        small.run(tier, T, C, 42, mbps=1000, mode="compute_only")
+        base = [small.read_chunk(s, C) for s in range(0, T, C)]
+        base_lg = small.logits()
+        for a, b in zip([_chunk_kv(small, s, C) for s in range(0, T, C)], full_kv):
+            assert rel(a, b) <= 2e-2
+        assert rel(base_lg, full) <= 2e-2
+        r = small.run(tier, T, C, 42, mbps=1000, mode="cake")
+        assert sorted(c.index for c in r.chunks) == list(range(T // C))
+        assert [small.read_chunk(s, C) for s in range(0, T, C)] == base
+        tier.close()
+    finally:
+        small.close()
