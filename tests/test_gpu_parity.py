@@ -17,6 +17,8 @@ CONFIGS = {
     "tiny": ((2, 256, 4, 4, 64, 1024, 32000), 2048, 256),
     "gqa_hd64": ((2, 512, 8, 2, 64, 1024, 32000), 1024, 256),
     "gqa_hd128": ((2, 1024, 8, 2, 128, 2048, 32768), 1024, 512),
+    # GQA 8:1 (the Llama-3-70B grouping: 16 tokens x 8 heads per 128-row tile)
+    "gqa8_hd128": ((2, 1024, 16, 2, 128, 2048, 32768), 1024, 256),
 }
 
 
