@@ -177,6 +177,21 @@ int g_gemm_schedule = 0;  // 0 whole tiles (+ exact split-K when tiles < SM pair
 int g_gemm_2sm = 1;       // 1: M > 128 projections use the 2-SM (cta_group::2) kernel
 int g_gemm_2sm_n128 = 0;  // experiment: O / down (N tiles of 128) on CTA pairs too
 int g_gemm_hints = 3;     // L2 policy of the operand loads (GemmArgs::l2_hints)
+int g_gemm_tail_split = 1;  // gate/up: split the short last round along K (swiglu_tail_kernel)
+
+// Tail-split partials of whole_tiles == 2 launches (stream-ordered reuse).
+float* g_tail_ws = nullptr;
+size_t g_tail_floats = 0;
+int tail_scratch(float** ws, size_t floats) {
+  std::lock_guard<std::mutex> lk(g_sk.mu);
+  if (floats > g_tail_floats) {
+    if (g_tail_ws) CK(cudaFree(g_tail_ws));
+    CK(cudaMalloc(&g_tail_ws, floats * sizeof(float)));
+    g_tail_floats = floats;
+  }
+  *ws = g_tail_ws;
+  return CAKE_OK;
+}
 
 int streamk_scratch(float** ws, int** flags, int* epoch) {
   std::lock_guard<std::mutex> lk(g_sk.mu);
@@ -310,9 +325,25 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
       ++split;
     a.whole_tiles = split == 1 ? 1 : 0;
     pairs = split == 1 ? std::min(tiles, max_pairs) : tiles * split;
+    // gate/up (224 tiles on 74 pairs at M = 512): the short last round split along K,
+    // its parts summed + SwiGLU'd by swiglu_tail_kernel
+    if constexpr (EPI == kEpiSwiglu && BLOCK_N == 256) {
+      const int r = tiles % pairs;
+      if (split == 1 && g_gemm_tail_split && tiles > pairs && r > 0 && 2 * r <= pairs && a.num_k_blocks >= 16) {
+        a.whole_tiles = 2;
+        CKS(tail_scratch(&a.tail_ws, static_cast<size_t>(r) * tail_parts(r, pairs) * 256 * 256));
+      }
+    }
   }
   CKS(streamk_scratch(&a.sk_ws, &a.sk_flags, &a.epoch));
   CK(launch_chain(kern, dim3(2 * pairs), dim3(kGemmThreads), Cfg::kSmemBytes, s, 2, ta, tb_half, a));
+  if constexpr (EPI == kEpiSwiglu) {
+    if (a.whole_tiles == 2) {
+      const int r = tiles % pairs;
+      CK(launch_chain(swiglu_tail_kernel, dim3(r * 256), dim3(128), 0, s, 1, a, tiles - r, r,
+                      tail_parts(r, pairs)));
+    }
+  }
   return CAKE_OK;
 }
 
@@ -1589,10 +1620,11 @@ int cake_kv_encode_q8(cake_model* m, const void* d_chunk, int chunk_len, void* d
 
 int cake_gemm_set_schedule(int schedule) {
   // bit 0: stream-K; bit 1: disable the 2-SM kernel; bit 2: 1-SM weight multicast clusters
-  if (schedule < 0 || schedule > 63)
+  if (schedule < 0 || schedule > 127)
     return fail(CAKE_EINVAL, "schedule bits: 1 stream-K, 2 no-2SM, 4 multicast, 8 2-SM for N-128 tiles");
   g_gemm_2sm_n128 = (schedule & 8) ? 1 : 0;
   g_gemm_hints = 3 ^ ((schedule >> 4) & 3);  // bits 4/5 drop the evict_last hint of A / B
+  g_gemm_tail_split = (schedule & 64) ? 0 : 1;  // bit 6: no tail split
   g_gemm_schedule = schedule & 1;
   g_gemm_2sm = (schedule & 2) ? 0 : 1;
   g_gemm_cluster = (schedule & 4) ? 1 : 0;

@@ -64,7 +64,10 @@ struct GemmArgs {
   float* sk_ws;             // [gridDim.x][128][BLOCK_N] partial tiles
   int* sk_flags;            // [gridDim.x] = epoch when the CTA's partial is published
   int epoch;
-  int whole_tiles;          // 1: classic persistent schedule (tile t -> CTA t % grid), no splits
+  int whole_tiles;          // 1: classic persistent schedule (tile t -> CTA t % grid), no splits;
+                            // 2: the same for the full rounds; the short last round is split along K,
+                            //    its parts land in tail_ws and a separate kernel sums them + epilogue
+  float* tail_ws;           // [tail tile][part][256 rows][256 cols] fp32 (whole_tiles == 2)
   int cs;                   // cluster size = CTAs sharing (multicasting) each weight k-block, one m-block each
   // RMSNorm folded into the projections. Producer side (kEpiResid): besides
   // h += acc, write bf16(h) (the next projection's A operand) and this tile's
@@ -100,30 +103,54 @@ struct GemmCfg {
 __device__ __forceinline__ float silu_f(float x) { return x / (1.0f + __expf(-x)); }
 
 // Contiguous unit range of one CTA and its walk over (tile, [kb0, kb1)) segments.
+// Mode 2 (tail split): whole tiles round-robin while every CTA gets one; each
+// of the r < grid leftover tiles is then cut along K into S = tail_parts(r, g)
+// parts on CTAs [t*S, t*S+S). The kernel ends after floor(tiles/grid) whole
+// tiles plus 1/S of one, instead of one more whole round (gate/up at M = 512:
+// 224 tiles on 74 pairs = 3 rounds + 2 tiles).
+constexpr int kTailSplit = 8;
+__host__ __device__ inline int tail_parts(int r, int g) { return r > 0 ? (g / r < kTailSplit ? g / r : kTailSplit) : 1; }
 struct StreamK {
   long long total, u, u_end;
   int nk, grid;
   int tile_mode = 0, next_tile = 0, n_tiles = 0;
+  int n_full = 0, tail_s = 1, cta_id = 0;
+  bool tail_done = false;
   __device__ StreamK(long long units, int num_k, int cta, int g, int whole_tiles = 0)
-      : total(units), nk(num_k), grid(g) {
+      : total(units), nk(num_k), grid(g), cta_id(cta) {
     u = units * cta / g;
     u_end = units * (cta + 1) / g;
     if (whole_tiles) {
-      tile_mode = 1;
+      tile_mode = whole_tiles;
       next_tile = cta;
       n_tiles = static_cast<int>(units / num_k);
+      n_full = whole_tiles == 2 ? n_tiles / g * g : n_tiles;
+      tail_s = tail_parts(n_tiles - n_full, g);
     }
   }
   // CTA that owns unit v under the balanced split
   __device__ int cta_of(long long v) const { return static_cast<int>(((v + 1) * grid + total - 1) / total - 1); }
   __device__ bool next(int& tile, int& kb0, int& kb1) {
     if (tile_mode) {
-      if (next_tile >= n_tiles) return false;
-      tile = next_tile;
-      next_tile += grid;
-      kb0 = 0;
-      kb1 = nk;
-      return true;
+      if (next_tile < n_full) {
+        tile = next_tile;
+        next_tile += grid;
+        kb0 = 0;
+        kb1 = nk;
+        return true;
+      }
+      if (tile_mode == 2 && !tail_done) {
+        tail_done = true;
+        const int r = n_tiles - n_full;
+        if (cta_id < r * tail_s) {
+          const int part = cta_id % tail_s;
+          tile = n_full + cta_id / tail_s;
+          kb0 = nk * part / tail_s;
+          kb1 = nk * (part + 1) / tail_s;
+          return true;
+        }
+      }
+      return false;
     }
     if (u >= u_end) return false;
     tile = static_cast<int>(u / nk);

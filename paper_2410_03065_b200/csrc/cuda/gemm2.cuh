@@ -164,6 +164,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     while (sk.next(tile, kb0, kb1)) {
       const int m = (tile % m_pairs) * 256 + static_cast<int>(rank) * 128 + row;
       const int n_blk = tile / m_pairs;
+      if (sk.tile_mode == 2 && tile >= sk.n_full) {
+        // a part of a tail tile: its fp32 accumulator goes to the tail workspace (row-major,
+        // 256 x BLOCK_N per part); gemm_tail_kernel sums the parts in order and applies the epilogue
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tbase =
+            tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + static_cast<uint32_t>(acc * BLOCK_N);
+        const int part = pair % sk.tail_s;
+        float* dst = args.tail_ws +
+                     (static_cast<size_t>((tile - sk.n_full) * sk.tail_s + part) * 256 + rank * 128 + row) * BLOCK_N;
+#pragma unroll 1
+        for (int c = 0; c < BLOCK_N / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c * 32, r);
+          tmem_ld_wait();
+          float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            __stcg(d4 + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                       __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
+        }
+        tc_fence_before();
+        mbar_arrive_cluster(leader_tempty0 + acc * 8);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+        continue;
+      }
       EpiPre<BLOCK_N, EPI> pre;
       pre.load(args, m, n_blk, kb0 > 0);
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -194,6 +223,43 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     tmem_dealloc_2sm<Cfg::kTmemCols>(tmem_base);
   }
+}
+
+// The tail tiles of a whole_tiles == 2 gate/up GEMM: out[m, j] = silu(g) * u
+// with g, u the sums (in part order) of the parts' accumulators, times the
+// fused-RMSNorm row scale. One CTA per (tail tile, row), one thread per
+// gate/up column pair; the row scale is reduced once per CTA.
+__global__ void __launch_bounds__(128) swiglu_tail_kernel(const GemmArgs a, int n_full, int n_tail_tiles, int parts) {
+  pdl_wait();
+  pdl_trigger();
+  if (a.abort_flag != nullptr && *(volatile const int*)a.abort_flag) return;
+  __shared__ float s_rs;
+  const int m_pairs = (a.num_m_blocks + 1) / 2;
+  const int t = blockIdx.x / 256, r = blockIdx.x % 256;
+  const int tile = n_full + t;
+  const int m = (tile % m_pairs) * 256 + r;
+  if (m >= a.M) return;
+  if (threadIdx.x < 32) {
+    float tt = 0.f;
+    if (a.ss_in != nullptr)
+      for (int q = threadIdx.x; q < a.ss_parts; q += 32) tt += __ldcg(a.ss_in + static_cast<size_t>(q) * a.ss_ld + m);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tt += __shfl_xor_sync(0xffffffffu, tt, o);
+    if (threadIdx.x == 0) s_rs = a.ss_in != nullptr ? rsqrtf(tt / static_cast<float>(a.rms_dim) + a.rms_eps) : 1.f;
+  }
+  const int j = threadIdx.x;
+  const float* src = a.tail_ws + (static_cast<size_t>(t) * parts * 256 + r) * 256;
+  float g = 0.f, u = 0.f;
+  for (int p = 0; p < parts; ++p) {
+    g += __ldcg(src + static_cast<size_t>(p) * 256 * 256 + j);
+    u += __ldcg(src + static_cast<size_t>(p) * 256 * 256 + 128 + j);
+  }
+  __syncthreads();
+  const float rs = s_rs;
+  g *= rs;
+  u *= rs;
+  reinterpret_cast<__nv_bfloat16*>(a.out)[static_cast<size_t>(m) * a.ldo + (tile / m_pairs) * 128 + j] =
+      __float2bfloat16_rn(silu_f(g) * u);
 }
 
 }  // namespace cake_dev
