@@ -62,6 +62,7 @@ struct FaArgs {
   int num_splits;
   float scale_log2;
   const int* abort_flag;
+  long long* trace;  // debug (nullptr): clock64 stamps of CTA (0,0,0), tools/attn_trace.py
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -221,11 +222,17 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
       constexpr uint32_t idesc_o = umma_idesc_bf16(kFaRows, HD, false, true);
       mbar_wait(q_ready, 0);
       tc_fence_after();
+      const bool trm = a.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+      if (trm) a.trace[0] = clock64(), a.trace[1] = nb;
       auto issue_pv = [&](int jj) {
         const int s = jj & 1;
         const int vs = jj % Cfg::kVStages;
+        if (trm && jj < 64) a.trace[64 + jj * 8 + 6] = clock64();
         mbar_wait(&p_ready[s], (jj >> 1) & 1);
+        if (trm && jj < 64) a.trace[64 + jj * 8 + 7] = clock64();
+        if (trm && jj < 64) a.trace[64 + 1024 + jj * 8] = clock64();
         mbar_wait(&v_full[vs], (jj / Cfg::kVStages) & 1);
+        if (trm && jj < 64) a.trace[64 + 1024 + jj * 8 + 1] = clock64();
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sV + vs * Cfg::kTileBytes);
         const uint32_t p_col = tmem + (s ? Cfg::kColS1 : Cfg::kColS0);
@@ -240,7 +247,9 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
       auto issue_s = [&](int jj) {
         const int s = jj & 1;
         const int ks = jj % Cfg::kKStages;
+        if (trm && jj < 64) a.trace[64 + 1024 + jj * 8 + 2] = clock64();
         mbar_wait(&k_full[ks], (jj / Cfg::kKStages) & 1);
+        if (trm && jj < 64) a.trace[64 + 1024 + jj * 8 + 3] = clock64();
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sK + ks * Cfg::kTileBytes);
         const uint32_t d = tmem + (s ? Cfg::kColS1 : Cfg::kColS0);
@@ -311,10 +320,15 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
       mbar_arrive(q_ready);
     }
     float m = -INFINITY, l = 0.f;
+    const bool tr = a.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && q4 == 0 &&
+                    lane == 0;
+    long long* trp = tr ? a.trace + 64 + g * 8 * 64 : nullptr;  // [group][block < 64][8]
     for (int j = 0; j < nb; ++j) {
       const int s = j & 1;
+      if (tr && j < 64) trp[j * 8] = clock64();
       mbar_wait(&s_full[s], (j >> 1) & 1);
       tc_fence_after();
+      if (tr && j < 64) trp[j * 8 + 1] = clock64();
       const uint32_t tS = tmem + lane_off + (s ? Cfg::kColS1 : Cfg::kColS0);
       float sv[kKeysPerG];
 #pragma unroll
@@ -333,11 +347,13 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
           if (key > qpos || key >= kmax_valid) sv[i] = -INFINITY;
         }
       }
+      if (tr && j < 64) trp[j * 8 + 2] = clock64();
       float mx = -INFINITY;
 #pragma unroll
       for (int i = 0; i < kKeysPerG; ++i) mx = fmaxf(mx, sv[i]);
       xmax[s][g][row] = mx;
       named_bar_sync(2, 128 * NG);
+      if (tr && j < 64) trp[j * 8 + 3] = clock64();
 #pragma unroll
       for (int h = 0; h < NG; ++h) mx = fmaxf(mx, xmax[s][h][row]);
       mx *= sc;  // scale > 0: max commutes
@@ -379,6 +395,7 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
         rs[i & 3] = fadd2(rs[i & 3], p);
         pk[i] = pack_bf16(p.x, p.y);
       }
+      if (tr && j < 64) trp[j * 8 + 4] = clock64();
       if constexpr (kKeysPerG / 2 == 32)
         tmem_st32(tS + g * 32, pk);
       else
@@ -388,6 +405,7 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_ready[s]);
+      if (tr && j < 64) trp[j * 8 + 5] = clock64();
     }
     // epilogue: total row sum, then this group's slice of O
     xsum[g][row] = l;

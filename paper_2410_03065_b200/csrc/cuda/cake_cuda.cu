@@ -682,6 +682,7 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
     fa.num_splits = splits;
     fa.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(m->hd));
     fa.abort_flag = abort_flag;
+    fa.trace = (g_fa4_trace_layer == layer) ? g_fa4_trace : nullptr;
     // two softmax groups (384 threads): four groups measured 10% slower at 32K (512-thread max exchange)
     if (m->hd == 128) {
       auto kern = attn_tc_kernel<128, 2>;
