@@ -197,45 +197,57 @@ __global__ void __launch_bounds__(kF4Threads, 1)
           }
         }
       }
-    } else if (warp == 1 && lane == 0 && nb > 0) {
+    } else if (warp == 1 && nb > 0) {
       // ------------------------------------------------ MMA issuer
+      // converged warp, one elected lane issues (see attn_tc_kernel: a
+      // single-lane issuer drains the tensor pipe at every barrier wait)
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(128, HD, false, true);
       mbar_wait(q_full, 0);
-      if (args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+      const bool tr = args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0;
+      if (tr) {
         args.trace[0] = clock64();
         args.trace[1] = nb;
       }
       auto issue_s = [&](int i, int j) {  // S_i = Q_i K(j)^T   (K(j) already waited for)
         const uint32_t q_addr = smem_u32(sQ + i * Cfg::kTileBytes);
         const uint32_t k_addr = smem_u32(sK + (j % Cfg::kKStages) * Cfg::kTileBytes);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * Cfg::kHalfBytes + (kk & 3) * 32;
-          umma_bf16_ss(tmem + i * 128, umma_desc_sw128(q_addr + off), umma_desc_sw128(k_addr + off), idesc_s,
-                       kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * Cfg::kHalfBytes + (kk & 3) * 32;
+            umma_bf16_ss(tmem + i * 128, umma_desc_sw128(q_addr + off), umma_desc_sw128(k_addr + off), idesc_s,
+                         kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[i]);
         }
-        umma_commit(&s_full[i]);
+        __syncwarp();
       };
-      const bool tr = args.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
       auto issue_pv = [&](int i, int j) {  // O_i += P_i V(j)   (V(j) already waited for)
         if (tr && j < 64) args.trace[64 + i * 8 * 64 + j * 8 + 6] = clock64();
         mbar_wait(&p_ready[i], j & 1);
         tc_fence_after();
         if (tr && j < 64) args.trace[64 + i * 8 * 64 + j * 8 + 7] = clock64();
         const uint32_t v_addr = smem_u32(sV + (j % Cfg::kVStages) * Cfg::kTileBytes);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 128 / 16; ++kk) {
-          const uint64_t bdesc = umma_desc_sw128_mn(v_addr + kk * 16 * 128, Cfg::kHalfBytes, 1024);
-          umma_bf16_ts(tmem + Cfg::kColO + i * HD, tmem + i * 128 + kk * 8, bdesc, idesc_o,
-                       (j > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < 128 / 16; ++kk) {
+            const uint64_t bdesc = umma_desc_sw128_mn(v_addr + kk * 16 * 128, Cfg::kHalfBytes, 1024);
+            umma_bf16_ts(tmem + Cfg::kColO + i * HD, tmem + i * 128 + kk * 8, bdesc, idesc_o,
+                         (j > 0 || kk > 0) ? 1u : 0u);
+          }
         }
+        __syncwarp();
+      };
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) umma_commit(bar);
+        __syncwarp();
       };
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
       issue_s(0, 0);
       issue_s(1, 0);
-      umma_commit(&k_empty[0]);
+      commit(&k_empty[0]);
       for (int j = 0; j < nb; ++j) {
         const bool more = j + 1 < nb;
         mbar_wait(&v_full[j % Cfg::kVStages], (j / Cfg::kVStages) & 1);
@@ -246,13 +258,13 @@ __global__ void __launch_bounds__(kF4Threads, 1)
           issue_s(0, j + 1);  // after PV0(j): S0(j+1) overwrites P0(j) in TMEM (in-order pipe)
         }
         issue_pv(1, j);
-        umma_commit(&v_empty[j % Cfg::kVStages]);
+        commit(&v_empty[j % Cfg::kVStages]);
         if (more) {
           issue_s(1, j + 1);
-          umma_commit(&k_empty[(j + 1) % Cfg::kKStages]);
+          commit(&k_empty[(j + 1) % Cfg::kKStages]);
         }
       }
-      umma_commit(o_final);
+      commit(o_final);
     }
   } else {
     setmaxnreg_inc<200>();

@@ -85,6 +85,9 @@ __device__ __forceinline__ float ex2_poly(float x) {
   p = fmaf(p, f, 0.99992811f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+#ifndef FA_POLY
+#define FA_POLY 2
+#endif
 // 2^x for a pair on the FMA pipe (ex2_poly on FFMA2 / FADD2).
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   x.x = fmaxf(x.x, -125.0f);
@@ -92,7 +95,7 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   const float2 big = make_float2(12582912.0f, 12582912.0f);
   const float2 t = fadd2(x, big);
   const float2 u = fadd2(t, make_float2(-12582912.0f, -12582912.0f));  // round(x)
-  const float2 f = make_float2(x.x - u.x, x.y - u.y);
+  const float2 f = ffma2(u, make_float2(-1.0f, -1.0f), x);  // x - round(x)
   float2 p = ffma2(make_float2(0.05517132f, 0.05517132f), f, make_float2(0.24261054f, 0.24261054f));
   p = ffma2(p, f, make_float2(0.69326099f, 0.69326099f));
   p = ffma2(p, f, make_float2(0.99992811f, 0.99992811f));
@@ -216,13 +219,17 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && nb > 0) {
+    if (nb > 0) {
       // ------------------------------------------------ MMA issuer
+      // The whole warp runs the loop (barrier waits on every lane) and one
+      // elected lane issues: a tcgen05.mma stream issued from a divergent
+      // single-lane branch drains the tensor pipe at every mbarrier wait
+      // (about 200 cycles each, three per block), a converged warp does not.
       constexpr uint32_t idesc_s = umma_idesc_bf16(kFaRows, kFaKeys, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(kFaRows, HD, false, true);
       mbar_wait(q_ready, 0);
       tc_fence_after();
-      const bool trm = a.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+      const bool trm = a.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0;
       if (trm) a.trace[0] = clock64(), a.trace[1] = nb;
       auto issue_pv = [&](int jj) {
         const int s = jj & 1;
@@ -236,13 +243,16 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
         tc_fence_after();
         const uint32_t v_addr = smem_u32(sV + vs * Cfg::kTileBytes);
         const uint32_t p_col = tmem + (s ? Cfg::kColS1 : Cfg::kColS0);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < kFaKeys / 16; ++kk) {
-          const uint64_t bdesc = umma_desc_sw128_mn(v_addr + kk * 16 * 128, Cfg::kHalfBytes, 1024);
-          umma_bf16_ts(tmem + Cfg::kColO, p_col + kk * 8, bdesc, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < kFaKeys / 16; ++kk) {
+            const uint64_t bdesc = umma_desc_sw128_mn(v_addr + kk * 16 * 128, Cfg::kHalfBytes, 1024);
+            umma_bf16_ts(tmem + Cfg::kColO, p_col + kk * 8, bdesc, idesc_o, (jj > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&v_empty[vs]);
+          umma_commit(pv_done);
         }
-        umma_commit(&v_empty[vs]);
-        umma_commit(pv_done);
+        __syncwarp();
       };
       auto issue_s = [&](int jj) {
         const int s = jj & 1;
@@ -253,13 +263,16 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sK + ks * Cfg::kTileBytes);
         const uint32_t d = tmem + (s ? Cfg::kColS1 : Cfg::kColS0);
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * Cfg::kHalfBytes + (kk & 3) * 32;
-          umma_bf16_ts(d, tmem + Cfg::kColQ + kk * 8, umma_desc_sw128(k_addr + off), idesc_s, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * Cfg::kHalfBytes + (kk & 3) * 32;
+            umma_bf16_ts(d, tmem + Cfg::kColQ + kk * 8, umma_desc_sw128(k_addr + off), idesc_s, kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[s]);
+          umma_commit(&k_empty[ks]);
         }
-        umma_commit(&s_full[s]);
-        umma_commit(&k_empty[ks]);
+        __syncwarp();
       };
       // S(j+1) is issued BEFORE waiting for P(j): the tensor pipe computes the
       // next block's scores while the softmax warps work on this one. (S(j+1)
@@ -269,7 +282,8 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
         if (j + 1 < nb) issue_s(j + 1);
         issue_pv(j);
       }
-      umma_commit(o_final);
+      if (elect_one()) umma_commit(o_final);
+      __syncwarp();
     }
   } else if (warp >= 4) {
     // ------------------------------------------------ softmax + epilogue
@@ -386,7 +400,7 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
       for (int i = 0; i < kKeysPerG / 2; ++i) {
         const float2 x = ffma2(make_float2(sv[2 * i], sv[2 * i + 1]), sc2, nb2);
         float2 p;
-        if ((i & 3) == 3) {  // every 4th pair on the FMA pipe: 25% of the exponentials off MUFU
+        if ((i & 7) >= 8 - FA_POLY) {  // FA_POLY of every 8 pairs on the FMA pipe, the rest on MUFU
           p = ex2_poly2(x);
         } else {
           p.x = ex2_approx(x.x);

@@ -492,8 +492,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {
       // ------------------------------------------------ MMA issuer
+      // The whole warp runs the schedule and waits; one elected lane issues.
+      // (A single-lane issuer in a divergent branch drains the tensor pipe at
+      // every full-barrier wait.)
       constexpr uint32_t idesc = umma_idesc_bf16(kGemmBlockM, BLOCK_N);
       StreamK sk(units, nk, cluster, n_clusters, args.whole_tiles);
       int stage = 0;
@@ -509,21 +512,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem_a + stage * Cfg::kABytes);
           const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kGemmBlockK / 16; ++k) {
-            umma_bf16_ss(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32),
-                         idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < kGemmBlockK / 16; ++k) {
+              umma_bf16_ss(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32),
+                           idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
+            if (cs > 1)
+              umma_commit_mc(&empty_bar[stage], mc_mask);
+            else
+              umma_commit(&empty_bar[stage]);
           }
-          if (cs > 1)
-            umma_commit_mc(&empty_bar[stage], mc_mask);
-          else
-            umma_commit(&empty_bar[stage]);
+          __syncwarp();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        umma_commit(&tfull_bar[acc]);
+        if (elect_one()) umma_commit(&tfull_bar[acc]);
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1u;

@@ -118,8 +118,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader) {
       // ------------------------------------------------ MMA issuer (leader only)
+      // converged warp, one elected lane issues (see gemm_tc_kernel)
       constexpr uint32_t idesc = umma_idesc_bf16(256, BLOCK_N);
       StreamK sk(units, nk, pair, n_pairs, args.whole_tiles);
       int stage = 0;
@@ -135,17 +136,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem_a + stage * Cfg::kABytes);
           const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::kBBytes);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kGemmBlockK / 16; ++k)
-            umma_bf16_ss_2sm(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32), idesc,
-                             (kb > kb0 || k > 0) ? 1u : 0u);
-          umma_commit_2sm_mc(&empty_bar[stage], 0x3);
+            for (int k = 0; k < kGemmBlockK / 16; ++k)
+              umma_bf16_ss_2sm(d_tmem, umma_desc_sw128(a_addr + k * 32), umma_desc_sw128(b_addr + k * 32), idesc,
+                               (kb > kb0 || k > 0) ? 1u : 0u);
+            umma_commit_2sm_mc(&empty_bar[stage], 0x3);
+          }
+          __syncwarp();
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        umma_commit_2sm_mc(&tfull_bar[acc], 0x3);
+        if (elect_one()) umma_commit_2sm_mc(&tfull_bar[acc], 0x3);
+        __syncwarp();
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1u;

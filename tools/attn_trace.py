@@ -34,3 +34,8 @@ for j in range(min(nb, 64)):
         print(f"{g} {j:3d} | {r[1]-r[0]:6d} {r[2]-r[1]:5d} {r[3]-r[2]:6d} {r[4]-r[3]:6d} {r[5]-r[4]:5d} | "
               f"{(tr[0][j][7]-tr[0][j][6]) if g == 0 else 0:6d} {(mm[j][1]-mm[j][0]) if g == 0 else 0:6d} "
               f"{(mm[j][3]-mm[j][2]) if g == 0 else 0:6d} | {r[0]-tr[0][0][0]}")
+print("MMA warp: cycles issuing S(j+1) MMAs (after K wait -> before P wait) and PV(j) MMAs (after V wait -> next K wait)")
+for j in range(min(nb, 64) - 2):
+    s_issue = tr[0][j][6] - mm[j + 1][3]
+    pv_issue = mm[j + 2][2] - mm[j][1]
+    print(f"{j:3d}  S-issue {s_issue:6d}  PV-issue {pv_issue:6d}")
