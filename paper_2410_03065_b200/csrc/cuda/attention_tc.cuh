@@ -222,9 +222,10 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
     if (nb > 0) {
       // ------------------------------------------------ MMA issuer
       // The whole warp runs the loop (barrier waits on every lane) and one
-      // elected lane issues: a tcgen05.mma stream issued from a divergent
-      // single-lane branch drains the tensor pipe at every mbarrier wait
-      // (about 200 cycles each, three per block), a converged warp does not.
+      // elected lane issues. In isolation a tcgen05.mma stream issued from a
+      // divergent single lane loses ~200 cycles at every mbarrier wait and a
+      // converged warp ~70 (profiles/r01_ncu_summary.md, "MMA issue"); in this
+      // kernel both measure the same block period (the softmax bounds it).
       constexpr uint32_t idesc_s = umma_idesc_bf16(kFaRows, kFaKeys, false, false);
       constexpr uint32_t idesc_o = umma_idesc_bf16(kFaRows, HD, false, true);
       mbar_wait(q_ready, 0);

@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     if (leader) {
       // ------------------------------------------------ MMA issuer (leader only)
-      // converged warp, one elected lane issues (see gemm_tc_kernel)
+      // converged warp, one elected lane issues (A/B against a lane-0 issuer: equal)
       constexpr uint32_t idesc = umma_idesc_bf16(256, BLOCK_N);
       StreamK sk(units, nk, pair, n_pairs, args.whole_tiles);
       int stage = 0;
