@@ -175,7 +175,7 @@ struct StreamKScratch {
 StreamKScratch g_sk;
 int g_gemm_schedule = 0;  // 0 whole tiles (+ exact split-K when tiles < SM pairs), 1 stream-K
 int g_gemm_2sm = 1;       // 1: M > 128 projections use the 2-SM (cta_group::2) kernel
-int g_gemm_2sm_n128 = 0;  // experiment: O / down (N tiles of 128) on CTA pairs too
+int g_gemm_2sm_n128 = 1;  // O / down (N tiles of 128) on CTA pairs: down 59.9 -> 54.0 us at M = 512
 int g_gemm_hints = 3;     // L2 policy of the operand loads (GemmArgs::l2_hints)
 int g_gemm_tail_split = 1;  // gate/up: split the short last round along K (swiglu_tail_kernel)
 
@@ -355,8 +355,9 @@ int gemm_dispatch(int bn, int epi, const CUtensorMap& ta, const CUtensorMap* tb3
   // MMA is M = 256 x N = bn, each CTA receiving its 128 rows of A and bn/2 rows
   // of the weight tile (24 KB per 64-deep k-block at bn = 128 instead of the
   // 1-SM tile's 32 KB: the M = 512 projections are bound by L2 -> SM delivery).
-  // At M = 512: QKV / gate-up 48 / 224 pair tiles of N 256. O / down stay on
-  // 1-SM 128 x 128 tiles: measured faster than pairs of N 128 (tools/gemm_sweep.py).
+  // At M = 512: QKV / gate-up 48 / 224 pair tiles of N 256, O / down 64 pair
+  // tiles of N 128 (down 54.0 us against 59.9 on 1-SM 128 x 128 tiles, O 20.8
+  // against 21.6; schedule bit 8 restores the 1-SM tiles).
   if (bn == 192) {
     if (a.M <= kGemmBlockM || a.N % bn) return fail(CAKE_EINVAL, "gemm: N-192 tiles need M > 128 and N %% 192 == 0");
     switch (epi) {
@@ -1622,8 +1623,8 @@ int cake_kv_encode_q8(cake_model* m, const void* d_chunk, int chunk_len, void* d
 int cake_gemm_set_schedule(int schedule) {
   // bit 0: stream-K; bit 1: disable the 2-SM kernel; bit 2: 1-SM weight multicast clusters
   if (schedule < 0 || schedule > 127)
-    return fail(CAKE_EINVAL, "schedule bits: 1 stream-K, 2 no-2SM, 4 multicast, 8 2-SM for N-128 tiles");
-  g_gemm_2sm_n128 = (schedule & 8) ? 1 : 0;
+    return fail(CAKE_EINVAL, "schedule bits: 1 stream-K, 2 no-2SM, 4 multicast, 8 1-SM N-128 tiles");
+  g_gemm_2sm_n128 = (schedule & 8) ? 0 : 1;
   g_gemm_hints = 3 ^ ((schedule >> 4) & 3);  // bits 4/5 drop the evict_last hint of A / B
   g_gemm_tail_split = (schedule & 64) ? 0 : 1;  // bit 6: no tail split
   g_gemm_schedule = schedule & 1;

@@ -1,9 +1,12 @@
 """cuBLAS (torch.matmul) on the four per-chunk projection shapes (M=512, bf16),
 CUDA-graph timed: the library reference point for the GEMM kernels."""
+import os
+
 import torch
 
 shapes = {"qkv": (512, 6144, 4096), "o": (512, 4096, 4096), "gu": (512, 28672, 4096), "down": (512, 4096, 14336)}
 for name, (M, N, K) in shapes.items():
+    M = int(os.environ.get("M", M))
     a = torch.randn(M, K, device="cuda").bfloat16()
     b = torch.randn(N, K, device="cuda").bfloat16()
     # weights larger than L2 in rotation so the weight stream comes from HBM as in the step

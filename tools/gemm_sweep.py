@@ -1,7 +1,8 @@
 """Projection GEMMs at M = 512 under each dispatch variant, CUDA-graph timed,
 weights rotated through > L2 worth of copies (as in the step, where every
 layer's weights stream from HBM). Variants = cake_gemm_set_schedule bits:
-1 stream-K, 2 no 2-SM (1-SM tiles), 4 1-SM weight-multicast clusters.
+1 stream-K, 2 no 2-SM (1-SM tiles), 4 1-SM weight-multicast clusters,
+8 O/down on 1-SM N-128 tiles instead of CTA pairs.
 
     python tools/gemm_sweep.py [variants=0,2,6,1] [shapes=qkv,o,gu,down]"""
 import ctypes
@@ -20,6 +21,7 @@ shapes = {"qkv": (512, 6144, 4096, 256), "qkv192": (512, 6144, 4096, 192), "gu19
           "down": (512, 4096, 14336, 128), "o256": (512, 4096, 4096, 256), "down256": (512, 4096, 14336, 256), "o1k": (1024, 4096, 4096, 128), "qkv1k": (1024, 6144, 4096, 256)}
 for name in names:
     M, N, K, bn = shapes[name]
+    M = int(os.environ.get("M", M))  # e.g. M=1024: two chunks per forward
     a = torch.randn(M, K, device="cuda").bfloat16()
     nb = max(2, int(400e6 // (N * K * 2)) + 1)
     bs = [torch.randn(N, K, device="cuda").bfloat16() for _ in range(nb)]
