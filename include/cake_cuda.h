@@ -221,7 +221,7 @@ CAKE_API int cake_model_launch_count(cake_model* m, long long* n, int reset);
  * (cta_group::2) kernel for M > 128, bit2 weight-multicast clusters in the
  * 1-SM kernel, bit3 N-128 tiles (O / down) on the 1-SM kernel instead of CTA
  * pairs, bits 4/5 drop the L2 evict_last hint of A / B, bit6 no K-split of
- * the short last gate/up round. Default 0. */
+ * the short last gate/up round, bit7 QKV on N-256 tiles instead of N-192. Default 0. */
 CAKE_API int cake_gemm_set_schedule(int schedule);
 /* C = A · B^T for bf16 row-major A [M, K], B [N, K]; epi 0: bf16 C, 1: fp32 C,
  * 2: fp32 C += . block_n 128 or 256. For tests and microbenchmarks. */

@@ -178,6 +178,7 @@ int g_gemm_2sm = 1;       // 1: M > 128 projections use the 2-SM (cta_group::2) 
 int g_gemm_2sm_n128 = 1;  // O / down (N tiles of 128) on CTA pairs: down 59.9 -> 54.0 us at M = 512
 int g_gemm_hints = 3;     // L2 policy of the operand loads (GemmArgs::l2_hints)
 int g_gemm_tail_split = 1;  // gate/up: split the short last round along K (swiglu_tail_kernel)
+int g_gemm_qkv192 = 1;      // QKV on CTA-pair tiles of N 192 (rope-unit weight rows) when the rows tile
 
 // Tail-split partials of whole_tiles == 2 launches (stream-ordered reuse).
 float* g_tail_ws = nullptr;
@@ -364,6 +365,7 @@ int gemm_dispatch(int bn, int epi, const CUtensorMap& ta, const CUtensorMap* tb3
       case kEpiBf16: return launch_gemm2<192, kEpiBf16>(ta, tb3[1], a, s);
       case kEpiF32: return launch_gemm2<192, kEpiF32>(ta, tb3[1], a, s);
       case kEpiResid: return launch_gemm2<192, kEpiResid>(ta, tb3[1], a, s);
+      case kEpiQkv: return launch_gemm2<192, kEpiQkv>(ta, tb3[1], a, s);
     }
     return fail(CAKE_EINVAL, "gemm: unsupported epi %d for N-192 tiles", epi);
   }
@@ -424,6 +426,7 @@ struct LayerWeights {
   bf16* ln1 = nullptr;
   bf16* ln2 = nullptr;
   CUtensorMap m_qkv[3], m_o[3], m_gu[3], m_d[3];  // B box = BLOCK_N / cluster size (1, 2, 4)
+  CUtensorMap m_qkv192[3];                         // QKV, box 96 rows (the pair kernel's N-192 halves)
 };
 
 struct ProfPair {
@@ -523,8 +526,9 @@ int alloc_dev(void** p, size_t bytes) {
 
 int init_tensor(bf16* dst, long long rows, long long cols, long long row_off, long long col_off,
                 long long logical_cols, long long group, long long group_stride, uint64_t seed,
-                uint32_t tid, float scale, cudaStream_t s) {
+                uint32_t tid, float scale, cudaStream_t s, int rope_hd = 0) {
   InitArgs a;
+  a.rope_hd = rope_hd;
   a.dst = dst;
   a.rows = rows;
   a.cols = cols;
@@ -951,7 +955,9 @@ int layer_attention_half(cake_model* m, int l, long long chunk_start, int M, con
     g.abort_flag = d_abort;
     if (g.N % m->bn_qkv) return fail(CAKE_EINVAL, "prefill: q-only pass needs tileable q rows");
     ProfScope ps(m, CAKE_K_GEMM_QKV, s, 2.0 * M * g.N * H, 2.0 * g.N * H + 2.0 * M * H + 2.0 * M * g.N);
-    CKS(gemm_dispatch(m->bn_qkv, kEpiQkv, m->a_xn, lw.m_qkv, g, s));
+    // N-192 pair tiles: 32 of them at M = 512 fill 64 SM pairs, against 24 of N 256 (24.1 vs 30.1 us)
+    const bool t192 = g_gemm_qkv192 && g_gemm_2sm && M > kGemmBlockM && g.N % 192 == 0;
+    CKS(gemm_dispatch(t192 ? 192 : m->bn_qkv, kEpiQkv, m->a_xn, t192 ? lw.m_qkv192 : lw.m_qkv, g, s));
   }
   CKS(attention(m, chunk_start, M, l, d_block_table, d_abort, s));
   return row_parallel(m, CAKE_K_GEMM_O, m->a_attn, lw.m_o, m->nq * m->hd, M, d_abort, s);
@@ -1207,6 +1213,10 @@ int cake_model_create(const cake_model_config* cfg, cake_model** out) {
   m->F = c.ffn / c.tp_size;
   m->qkv_rows = (m->nq + 2 * m->nkv) * m->hd;
   m->bn_qkv = (m->qkv_rows % 256 == 0) ? 256 : 128;
+  if (m->hd % 64) {
+    delete m;
+    return fail(CAKE_EINVAL, "model: head_dim %d is not a multiple of 64 (rope-unit QKV rows)", m->hd);
+  }
   if (m->qkv_rows % m->bn_qkv) {
     delete m;
     return fail(CAKE_EINVAL, "model: qkv rows %d not tileable", m->qkv_rows);
@@ -1246,11 +1256,14 @@ int cake_model_create(const cake_model_config* cfg, cake_model** out) {
     lw.ln1 = take(H);
     lw.ln2 = take(H);
     const long long qrows = static_cast<long long>(m->nq) * hd, kvrows = static_cast<long long>(m->nkv) * hd;
-    if ((st = init_tensor(lw.wqkv, qrows, H, r * qrows, 0, H, 0, 0, seed, tid_layer(l, kWq), s_h, s))) return bail(st);
-    if ((st = init_tensor(lw.wqkv + qrows * H, kvrows, H, r * kvrows, 0, H, 0, 0, seed, tid_layer(l, kWk), s_h, s)))
+    // QKV rows in rope-unit order within each head (qkv_row_of, elementwise.cuh)
+    if ((st = init_tensor(lw.wqkv, qrows, H, r * qrows, 0, H, 0, 0, seed, tid_layer(l, kWq), s_h, s, hd)))
+      return bail(st);
+    if ((st = init_tensor(lw.wqkv + qrows * H, kvrows, H, r * kvrows, 0, H, 0, 0, seed, tid_layer(l, kWk), s_h, s,
+                          hd)))
       return bail(st);
     if ((st = init_tensor(lw.wqkv + (qrows + kvrows) * H, kvrows, H, r * kvrows, 0, H, 0, 0, seed,
-                          tid_layer(l, kWv), s_h, s)))
+                          tid_layer(l, kWv), s_h, s, hd)))
       return bail(st);
     if ((st = init_tensor(lw.wo, H, m->nq * hd, 0, r * qrows, c.n_heads * hd, 0, 0, seed, tid_layer(l, kWo), s_o, s)))
       return bail(st);
@@ -1269,6 +1282,7 @@ int cake_model_create(const cake_model_config* cfg, cake_model** out) {
     for (int ci = 0; ci < 3; ++ci) {
       const uint32_t div = 1u << ci;  // cluster size 1, 2, 4
       if ((st = make_map(&lw.m_qkv[ci], lw.wqkv, m->qkv_rows, H, m->bn_qkv / div))) return bail(st);
+      if (m->qkv_rows % 192 == 0 && (st = make_map(&lw.m_qkv192[ci], lw.wqkv, m->qkv_rows, H, 96))) return bail(st);
       if ((st = make_map(&lw.m_o[ci], lw.wo, H, m->nq * hd, 128 / div))) return bail(st);
       if ((st = make_map(&lw.m_gu[ci], lw.wgu, 2 * F, H, 256 / div))) return bail(st);
       if ((st = make_map(&lw.m_d[ci], lw.wd, H, F, 128 / div))) return bail(st);
@@ -1622,8 +1636,9 @@ int cake_kv_encode_q8(cake_model* m, const void* d_chunk, int chunk_len, void* d
 
 int cake_gemm_set_schedule(int schedule) {
   // bit 0: stream-K; bit 1: disable the 2-SM kernel; bit 2: 1-SM weight multicast clusters
-  if (schedule < 0 || schedule > 127)
-    return fail(CAKE_EINVAL, "schedule bits: 1 stream-K, 2 no-2SM, 4 multicast, 8 1-SM N-128 tiles");
+  if (schedule < 0 || schedule > 255)
+    return fail(CAKE_EINVAL, "schedule bits: 1 stream-K, 2 no-2SM, 4 multicast, 8 1-SM N-128 tiles, 128 no QKV N-192");
+  g_gemm_qkv192 = (schedule & 128) ? 0 : 1;
   g_gemm_2sm_n128 = (schedule & 8) ? 0 : 1;
   g_gemm_hints = 3 ^ ((schedule >> 4) & 3);  // bits 4/5 drop the evict_last hint of A / B
   g_gemm_tail_split = (schedule & 64) ? 0 : 1;  // bit 6: no tail split

@@ -31,11 +31,23 @@ __host__ __device__ __forceinline__ float weight_value(uint64_t seed, uint32_t t
 // physical column c to logical column c + col_off of a [*, logical_cols]
 // tensor. group/group_stride express the gate|up interleave of the fused
 // MLP-in weight (group = 128 rows of one tensor per 256-row block).
+// QKV weight rows are stored in "rope units" inside each head: unit j (64 rows)
+// holds canonical rows [32j, 32j+32) followed by their RoPE partners
+// [hd/2 + 32j, hd/2 + 32j + 32). Any 64-multiple column tile of the QKV GEMM
+// then holds whole rotation pairs, so the fused RoPE epilogue works on 192-wide
+// tiles (32 tile pairs at M = 512 instead of 24). hd = 64 is the identity.
+// Maps a physical row within the head to its canonical row.
+__host__ __device__ __forceinline__ int qkv_row_of(int p, int hd) {
+  const int j = p >> 6, t = p & 63;
+  return t < 32 ? j * 32 + t : (hd >> 1) + j * 32 + (t - 32);
+}
+
 struct InitArgs {
   __nv_bfloat16* dst;
   long long rows, cols, dst_ld;
   long long row_off, col_off, logical_cols;
   long long group, group_stride;  // group = 0: identity row map
+  int rope_hd;                    // > 0: QKV rows in rope-unit order within each head (see qkv_row_of)
   uint64_t seed;
   uint32_t tensor_id;
   float scale;
@@ -47,6 +59,7 @@ __global__ void init_weight_kernel(const InitArgs a) {
        i += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long r = i / a.cols, c = i % a.cols;
     long long lr = r;
+    if (a.rope_hd > 0) lr = (r / a.rope_hd) * a.rope_hd + qkv_row_of(static_cast<int>(r % a.rope_hd), a.rope_hd);
     if (a.group > 0) lr = (r / a.group) * a.group_stride + (r % a.group);
     lr += a.row_off;
     const uint64_t li = static_cast<uint64_t>(lr) * a.logical_cols + (c + a.col_off);

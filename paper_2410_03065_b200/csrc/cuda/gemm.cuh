@@ -330,20 +330,25 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t tba
         }
       }
     } else if constexpr (EPI == kEpiQkv) {
+      // rows of the QKV weight are in rope-unit order (qkv_row_of): tile column
+      // block [64u, 64u + 64) holds a head's canonical columns [32j, 32j + 32) and
+      // their rotation partners [hd/2 + 32j, ...), with j = unit % (hd / 64)
+      static_assert(BLOCK_N % 64 == 0, "QKV tiles hold whole rope units");
       const int hd = args.head_dim;
       const int half = hd >> 1;
-      const int heads_per_tile = BLOCK_N / hd;
+      const int units_per_head = hd >> 6;
       const long long pos = args.pos0 + m;
 #pragma unroll 1
-      for (int h = 0; h < heads_per_tile; ++h) {
-        const int head = n_blk * heads_per_tile + h;
+      for (int k = 0; k < BLOCK_N / 64; ++k) {
+        const int unit = n_blk * (BLOCK_N / 64) + k;
+        const int head = unit / units_per_head;
+        const int j = unit % units_per_head;
         const int region =
             head < args.n_q_heads ? 0 : (head < args.n_q_heads + args.n_kv_heads ? 1 : 2);
-#pragma unroll 1
-        for (int j = 0; j < half / 32; ++j) {
+        {
           uint32_t x0[32], x1[32];
-          load_acc(h * hd + j * 32, x0);
-          load_acc(h * hd + half + j * 32, x1);
+          load_acc(k * 64, x0);
+          load_acc(k * 64 + 32, x1);
           if (!valid) continue;
           float o0[32], o1[32];
           if (region < 2) {

@@ -137,8 +137,10 @@ __global__ void __launch_bounds__(kSkinnyWarps * 32) skinny_kernel(const SkinnyA
     } else if constexpr (EPI == kSkQRope) {
       const int half = a.head_dim >> 1;
       const int head = u / half, i = u % half;
-      const int r0 = head * a.head_dim + i;
-      const __nv_bfloat16* w[2] = {a.W + static_cast<size_t>(r0) * a.K, a.W + static_cast<size_t>(r0 + half) * a.K};
+      const int r0 = head * a.head_dim + i;  // canonical q column
+      // physical weight rows: rope-unit order (qkv_row_of): i -> 64 (i / 32) + i % 32, its partner 32 later
+      const int p0 = head * a.head_dim + (i >> 5) * 64 + (i & 31);
+      const __nv_bfloat16* w[2] = {a.W + static_cast<size_t>(p0) * a.K, a.W + static_cast<size_t>(p0 + 32) * a.K};
       float acc[2][4];
       skinny_dot<2>(w, xs, a.M, a.K, acc);
       if (lane == 0)
