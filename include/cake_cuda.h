@@ -125,7 +125,8 @@ CAKE_API int cake_model_destroy(cake_model* m);
 CAKE_API int cake_model_get_info(const cake_model* m, cake_model_info* out);
 /* Attention kernel variant: 0 = product dispatch (the one-tile tcgen05/TMEM
  * flash attention kernel), 1 = mma.sync flash attention (independent
- * cross-check), 2 / 3 = the one-tile / two-tile tcgen05 kernel (tests). */
+ * cross-check), 2 / 3 = the one-tile / two-tile tcgen05 kernel (tests), 4 = the
+ * one-tile kernel with decoupled softmax groups (attention_dec.cuh). */
 CAKE_API int cake_model_set_attention_impl(cake_model* m, int impl);
 /* NCCL plumbing for head-sharded TP (one process per GPU): rank 0 makes the
  * 128-byte id, the launcher broadcasts it, every rank inits its communicator. */

@@ -363,9 +363,13 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
         }
       }
       if (tr && j < 64) trp[j * 8 + 2] = clock64();
-      float mx = -INFINITY;
+      // row max over 8 independent chains (a single chain is kKeysPerG dependent FMNMX)
+      float mc[8];
 #pragma unroll
-      for (int i = 0; i < kKeysPerG; ++i) mx = fmaxf(mx, sv[i]);
+      for (int c = 0; c < 8; ++c) mc[c] = sv[c];
+#pragma unroll
+      for (int i = 8; i < kKeysPerG; ++i) mc[i & 7] = fmaxf(mc[i & 7], sv[i]);
+      float mx = fmaxf(fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])), fmaxf(fmaxf(mc[4], mc[5]), fmaxf(mc[6], mc[7])));
       xmax[s][g][row] = mx;
       named_bar_sync(2, 128 * NG);
       if (tr && j < 64) trp[j * 8 + 3] = clock64();

@@ -19,6 +19,7 @@
 #include "attention.cuh"
 #include "attention_tc.cuh"
 #include "attention_fa4.cuh"
+#include "attention_dec.cuh"
 #include "cake_cuda.h"
 #include "elementwise.cuh"
 #include "gemm.cuh"
@@ -688,8 +689,26 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
     fa.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(m->hd));
     fa.abort_flag = abort_flag;
     fa.trace = (g_fa4_trace_layer == layer) ? g_fa4_trace : nullptr;
-    // two softmax groups (384 threads): four groups measured 10% slower at 32K (512-thread max exchange)
-    if (m->hd == 128) {
+    if (m->attn_impl == 4) {  // decoupled softmax groups (attention_dec.cuh)
+      if (m->hd == 128) {
+        auto kern = attn_dec_kernel<128>;
+        static bool cfgd = false;
+        if (!cfgd) {
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FdCfg<128>::kSmem));
+          cfgd = true;
+        }
+        CK(launch_chain(kern, grid, dim3(fa_threads<2>()), FdCfg<128>::kSmem, s, 1, m->tm_q, m->tm_kv, fa));
+      } else {
+        auto kern = attn_dec_kernel<64>;
+        static bool cfgd = false;
+        if (!cfgd) {
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FdCfg<64>::kSmem));
+          cfgd = true;
+        }
+        CK(launch_chain(kern, grid, dim3(fa_threads<2>()), FdCfg<64>::kSmem, s, 1, m->tm_q, m->tm_kv, fa));
+      }
+    } else if (m->hd == 128) {
+      // two softmax groups (384 threads): four groups measured 10% slower at 32K (512-thread max exchange)
       auto kern = attn_tc_kernel<128, 2>;
       static bool cfgd = false;
       if (!cfgd) {
@@ -1409,9 +1428,9 @@ CAKE_API int cake_debug_fa4_trace(void* dev_buf, int layer) {
 }
 
 int cake_model_set_attention_impl(cake_model* m, int impl) {
-  if (impl < 0 || impl > 3)
-    return fail(CAKE_EINVAL, "attention impl must be 0 (product dispatch), 1 (mma.sync), 2 (one-tile tcgen05) "
-                             "or 3 (two-tile tcgen05)");
+  if (impl < 0 || impl > 4)
+    return fail(CAKE_EINVAL, "attention impl must be 0 (product dispatch), 1 (mma.sync), 2 (one-tile tcgen05), "
+                             "3 (two-tile tcgen05) or 4 (one-tile, decoupled softmax groups)");
   m->attn_impl = impl;
   return CAKE_OK;
 }

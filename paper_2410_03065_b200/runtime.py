@@ -138,7 +138,8 @@ class GpuRuntime:
         """"tcgen05" (product dispatch), "tcgen05_1tile" / "tcgen05_2tile" (one tcgen05
         kernel for every chunk) or "mma_sync" (independent cross-check kernel)."""
         self.n.call("cake_gpu_set_attention_impl", self.h,
-                    {"tcgen05": 0, "mma_sync": 1, "tcgen05_1tile": 2, "tcgen05_2tile": 3}[impl])
+                    {"tcgen05": 0, "mma_sync": 1, "tcgen05_1tile": 2, "tcgen05_2tile": 3,
+                     "tcgen05_dec": 4}[impl])
 
     def set_profiling(self, kernels="all", stride: int = 1):
         """Bracket launches of the named kernel classes with CUDA events ("all", None, or a list);

@@ -31,7 +31,7 @@ def gpu():
         pytest.skip("no GPU")
 
 
-@pytest.mark.parametrize("impl", ["tcgen05", "tcgen05_2tile"])
+@pytest.mark.parametrize("impl", ["tcgen05", "tcgen05_2tile", "tcgen05_dec"])
 def test_8b_two_layers_vs_oracle(gpu, impl):
     """Product dispatch, and the two-tile attention kernel forced for every chunk."""
     import llama_oracle

@@ -132,14 +132,16 @@ def test_tcgen05_attention_matches_mma_sync_kernel(setup):
     assert rel(rt.logits(), lg_mma) <= 2e-2
 
 
-def test_two_tile_attention_matches_one_tile_kernel(setup):
-    """The two-tile (ping-pong) tcgen05 kernel against the one-tile tcgen05 kernel."""
+@pytest.mark.parametrize("other", ["tcgen05_2tile", "tcgen05_dec"])
+def test_two_tile_attention_matches_one_tile_kernel(setup, other):
+    """The two-tile (ping-pong) tcgen05 kernel, and the one-tile kernel with
+    decoupled softmax groups, against the one-tile tcgen05 kernel."""
     rt, T, C = setup["rt"], setup["T"], setup["C"]
     rt.set_attention_impl("tcgen05_1tile")
     rt.run(setup["tier"], T, C, 42, mbps=1000, mode="compute_only")
     one = [_chunk_kv(rt, s, C) for s in range(0, T, C)]
     lg_one = rt.logits()
-    rt.set_attention_impl("tcgen05_2tile")
+    rt.set_attention_impl(other)
     rt.run(setup["tier"], T, C, 42, mbps=1000, mode="compute_only")
     two = [_chunk_kv(rt, s, C) for s in range(0, T, C)]
     lg_two = rt.logits()

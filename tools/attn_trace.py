@@ -17,7 +17,7 @@ T = int(os.environ.get("T", "8192"))
 lib = native.load_cuda()
 buf = torch.zeros(64 + 3 * 64 * 8, dtype=torch.int64, device="cuda")
 rt = GpuRuntime("llama3_8b", max_tokens=T, max_chunk=512)
-rt.set_attention_impl("tcgen05_1tile")
+rt.set_attention_impl(os.environ.get("IMPL", "tcgen05_1tile"))
 lib.cake_debug_fa4_trace(ctypes.c_void_p(buf.data_ptr()), 5)
 rt.build_cache_tier(T, 512, 42)
 torch.cuda.synchronize()
