@@ -763,13 +763,13 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
   }
   if (splits > 1) {
     const int rows = chunk_len * m->nq;
-    const int wpb = 8;
+    if (splits > kCombineMaxSplits) return fail(CAKE_EINVAL, "attention: %d splits > %d", splits, kCombineMaxSplits);
     if (m->hd == 128)
-      CK(launch_chain(attn_combine_kernel<128>, dim3((rows + wpb - 1) / wpb), dim3(wpb * 32), 0, s, 1,
+      CK(launch_chain(attn_combine_kernel<128>, dim3(rows), dim3(128), 0, s, 1,
                       static_cast<const float*>(m->part_o), static_cast<const float*>(m->part_lse), m->attn, rows,
                       splits, abort_flag));
     else
-      CK(launch_chain(attn_combine_kernel<64>, dim3((rows + wpb - 1) / wpb), dim3(wpb * 32), 0, s, 1,
+      CK(launch_chain(attn_combine_kernel<64>, dim3(rows), dim3(64), 0, s, 1,
                       static_cast<const float*>(m->part_o), static_cast<const float*>(m->part_lse), m->attn, rows,
                       splits, abort_flag));
     CKL();
