@@ -41,8 +41,10 @@ struct SkinnyArgs {
 
 constexpr int kSkinnyWarps = 8;
 // dot-loop unroll (16-B loads in flight per row and lane). A/B on the
-// first-token step: 2 / 4 / 8 -> 5.42 / 5.44 / 5.38 ms; an L2 prefetch of each
-// warp's first rows before the PDL wait measured slower (5.76 ms).
+// first-token step: 2 / 4 / 8 -> 5.42 / 5.44 / 5.38 ms. Touching the weights
+// before the PDL wait measured slower: an L2 prefetch of each warp's first rows
+// 5.76 ms, a register preload of its first 4 / 8 batches 6.99 / 8.72 ms (the
+// early loads compete with the still-running memory-bound predecessor).
 constexpr int kSkinnyUnroll = 8;
 
 template <int NR>
