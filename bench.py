@@ -26,6 +26,17 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "TTFT ms at 32K ctx (Llama-3-8B shape) vs compute-only/IO-only; chunks/s"
+
+
+def workload_config(T, C, mbps, world):
+    """The `config` object of both arms' JSON lines (same workload)."""
+    return {"workload": f"llama3-8b-shape T={T} chunk={C} tier=pinned-DRAM link={mbps}mbps "
+                        f"({mbps / 8000:g} GB/s) bidirectional+race", "model": "llama-3-8b-shape", "seq_len": T,
+            "chunk": C, "link_mbps": mbps,
+            "parallelism": f"tp{world} (KV-head sharded, NCCL all-reduce)" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (16 GB weights, 4 GiB KV tier) — no flush"}
+
+
 DIMS_8B = (32, 4096, 32, 8, 128, 14336, 128256)
 
 
@@ -193,9 +204,9 @@ def reference_arm(args):
     v = statistics.mean(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"llama3-8b-shape T={args.tokens} chunk={args.chunk} link={args.mbps}mbps "
-                                   f"(bidirectional, CPU)"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": dict(workload_config(args.tokens, args.chunk, args.mbps, 1),
+                           parallelism=f"host CPU, {last['cores']} threads (reference scheduler + CPU Llama forward)"),
             "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -320,11 +331,7 @@ def b200_arm(args):
         "metric": METRIC, "value": dev, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": wall, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init Llama-3-8B-shape weights, seeded prompt)",
-        "config": {"workload": f"llama3-8b-shape T={T} chunk={C} tier=pinned-DRAM link={mbps}mbps "
-                               f"(8 GB/s) bidirectional+race", "model": "llama-3-8b-shape", "seq_len": T,
-                   "chunk": C, "link_mbps": mbps,
-                   "parallelism": f"tp{world} (KV-head sharded, NCCL all-reduce)" if world > 1 else "1 GPU",
-                   "l2": "inputs larger than L2 (16 GB weights, 4 GiB KV tier) — no flush"},
+        "config": workload_config(T, C, mbps, world),
         "ttft_compute_only_ms": base_c.device_ttft_ms, "ttft_io_only_ms": base_io.device_ttft_ms,
         "ttft_vs_min_baseline": dev / min(base_c.device_ttft_ms, base_io.device_ttft_ms),
         "chunks_per_s": last.n_chunks / (dev / 1e3), "merge_point": last.merge_point, "n_chunks": last.n_chunks,
