@@ -21,6 +21,13 @@
 
 namespace cake_dev {
 
+// DEC_SPLIT_S = 1 measured slower (block period 1973 vs 1621 cycles at 32K):
+// with Q in shared memory an N = 64 SS MMA reads 6 KB per 32 cycles, above the
+// 128 B/clk shared-memory port, and the split serialises the groups' S.
+#ifndef DEC_SPLIT_S
+#define DEC_SPLIT_S 0
+#endif
+
 template <int HD>
 struct FdCfg {
   static constexpr int kHalves = HD / 64;
@@ -69,11 +76,11 @@ __global__ void __launch_bounds__(fa_threads<2>(), 1)
   uint64_t* k_empty = bar + 4;    // [3]
   uint64_t* v_full = bar + 7;     // [2]
   uint64_t* v_empty = bar + 9;    // [2]
-  uint64_t* s_full = bar + 11;    // [2]
-  uint64_t* p_ready = bar + 13;   // [2 buffers][2 groups]
-  uint64_t* pv_done = bar + 17;   // [2 groups]
-  uint64_t* o_final = bar + 19;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
+  uint64_t* s_full = bar + 11;    // [2 buffers][2 groups]
+  uint64_t* p_ready = bar + 15;   // [2 buffers][2 groups]
+  uint64_t* pv_done = bar + 19;   // [2 groups]
+  uint64_t* o_final = bar + 21;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 22);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_kv);
@@ -86,7 +93,7 @@ __global__ void __launch_bounds__(fa_threads<2>(), 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) mbar_init(&s_full[s], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
     for (int i = 0; i < 4; ++i) mbar_init(&p_ready[i], 128);
     mbar_init(&pv_done[0], 1);
     mbar_init(&pv_done[1], 1);
@@ -157,21 +164,27 @@ __global__ void __launch_bounds__(fa_threads<2>(), 1)
       const uint32_t q_addr = smem_u32(sQ);
       const bool trm = a.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0;
       if (trm) a.trace[0] = clock64(), a.trace[1] = nb;
-      auto issue_s = [&](int jj) {
+      // DEC_SPLIT_S: S(j) as two N = 64 MMAs, one per group's keys, issued
+      // between the PVs so the two groups start their blocks at different times
+      // (their phases then overlap on each sub-partition); else one N = 128 MMA.
+      constexpr uint32_t idesc_s64 = umma_idesc_bf16(kFaRows, kFaKeys / 2, false, false);
+      auto issue_s = [&](int jj, int g) {  // g < 0: both halves as one N = 128 MMA
         const int s = jj & 1;
         const int ks = jj % Cfg::kKStages;
-        mbar_wait(&k_full[ks], (jj / Cfg::kKStages) & 1);
+        if (g <= 0) mbar_wait(&k_full[ks], (jj / Cfg::kKStages) & 1);
         tc_fence_after();
-        const uint32_t k_addr = smem_u32(sK + ks * Cfg::kTileBytes);
-        const uint32_t d = tmem + (s ? Cfg::kColS1 : Cfg::kColS0);
+        const uint32_t k_addr = smem_u32(sK + ks * Cfg::kTileBytes) + (g > 0 ? Cfg::kPageHalfBytes : 0);
+        const uint32_t d = tmem + (s ? Cfg::kColS1 : Cfg::kColS0) + (g > 0 ? kFaKeys / 2 : 0);
         if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < HD / 16; ++kk) {
             const uint32_t off = (kk >> 2) * Cfg::kHalfBytes + (kk & 3) * 32;
-            umma_bf16_ss(d, umma_desc_sw128(q_addr + off), umma_desc_sw128(k_addr + off), idesc_s, kk > 0 ? 1u : 0u);
+            umma_bf16_ss(d, umma_desc_sw128(q_addr + off), umma_desc_sw128(k_addr + off), g < 0 ? idesc_s : idesc_s64,
+                         kk > 0 ? 1u : 0u);
           }
-          umma_commit(&s_full[s]);
-          umma_commit(&k_empty[ks]);
+          if (g <= 0) umma_commit(&s_full[s * 2]);
+          if (g != 0) umma_commit(&s_full[s * 2 + 1]);
+          if (g != 0) umma_commit(&k_empty[ks]);
         }
         __syncwarp();
       };
@@ -197,11 +210,22 @@ __global__ void __launch_bounds__(fa_threads<2>(), 1)
       };
       // S(j+1) before PV(j): the pipe computes the next scores while the groups
       // finish P(j). S(j+1) overwrites P(j-1), whose PVs were issued before it.
-      issue_s(0);
-      for (int j = 0; j < nb; ++j) {
-        if (j + 1 < nb) issue_s(j + 1);
-        issue_pv(j, 0);
-        issue_pv(j, 1);
+      if (DEC_SPLIT_S) {
+        issue_s(0, 0);
+        issue_s(0, 1);
+        for (int j = 0; j < nb; ++j) {
+          if (j + 1 < nb) issue_s(j + 1, 0);
+          issue_pv(j, 0);
+          if (j + 1 < nb) issue_s(j + 1, 1);
+          issue_pv(j, 1);
+        }
+      } else {
+        issue_s(0, -1);
+        for (int j = 0; j < nb; ++j) {
+          if (j + 1 < nb) issue_s(j + 1, -1);
+          issue_pv(j, 0);
+          issue_pv(j, 1);
+        }
       }
       if (elect_one()) umma_commit(o_final);
       __syncwarp();
@@ -255,7 +279,7 @@ __global__ void __launch_bounds__(fa_threads<2>(), 1)
     for (int j = 0; j < nb; ++j) {
       const int s = j & 1;
       if (tr && j < 64) trp[j * 8] = clock64();
-      mbar_wait(&s_full[s], (j >> 1) & 1);
+      mbar_wait(&s_full[s * 2 + g], (j >> 1) & 1);
       tc_fence_after();
       if (tr && j < 64) trp[j * 8 + 1] = clock64();
       const uint32_t tS = tmem + lane_off + (s ? Cfg::kColS1 : Cfg::kColS0);
