@@ -10,6 +10,8 @@ from paper_2410_03065_b200.runtime import GpuRuntime  # noqa: E402
 T = int(os.environ.get("T", "32768"))
 rt = GpuRuntime("llama3_8b", max_tokens=T, max_chunk=512)
 tier = rt.build_cache_tier(T, 512, 42)
+if os.environ.get("IMPL"):
+    rt.set_attention_impl(os.environ["IMPL"])
 for _ in range(2):
     r = rt.run(tier, T, 512, 42, mbps=256000, mode="io_only")
 print(f"unprofiled: final step {r.final_step_ms:.3f} ms, kv resident {r.kv_resident_ms:.2f} ms")
