@@ -42,10 +42,11 @@ struct SkinnyArgs {
 constexpr int kSkinnyWarps = 8;
 // dot-loop unroll (16-B loads in flight per row and lane). A/B on the
 // first-token step: 2 / 4 / 8 -> 5.42 / 5.44 / 5.38 ms; 16 (with 8 CTAs per SM)
-// 5.29 ms. Touching the weights
-// before the PDL wait measured slower: an L2 prefetch of each warp's first rows
-// 5.76 ms, a register preload of its first 4 / 8 batches 6.99 / 8.72 ms (the
-// early loads compete with the still-running memory-bound predecessor).
+// 5.29 ms. Touching the weights before the PDL wait measured slower: an L2
+// prefetch of each warp's first rows 5.76 ms, a register preload of its first
+// 4 / 8 batches 6.99 / 8.72 ms (the early loads compete with the still-running
+// memory-bound predecessor). Two warps per row of the long-K down projection
+// (K halves summed in order) measured within noise (5.23 vs 5.27 ms).
 constexpr int kSkinnyUnroll = 16;
 
 template <int NR>
