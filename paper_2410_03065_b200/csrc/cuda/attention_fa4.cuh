@@ -49,6 +49,13 @@
 #include "attention_tc.cuh"
 #include "ptx.cuh"
 
+// pairs of every 8 exponentials on the FMA pipe; round (cycles) at 32K for 0..5:
+// 3391 / 3270 / 3167-3210 / 3404 / 3521 / 3659 (the one-tile kernel: FA_POLY,
+// 0 / 1 / 2 -> 1696 / 1613 / 1622)
+#ifndef FA4_POLY
+#define FA4_POLY 2
+#endif
+
 namespace cake_dev {
 
 constexpr int kF4Threads = 384;
@@ -347,7 +354,7 @@ __global__ void __launch_bounds__(kF4Threads, 1)
       for (int w = 0; w < 64; ++w) {
         const float2 x = ffma2(make_float2(__uint_as_float(su[2 * w]), __uint_as_float(su[2 * w + 1])), sc2, nb2);
         float2 p;
-        if ((w & 3) == 3) {
+        if ((w & 7) >= 8 - FA4_POLY) {  // FA4_POLY of every 8 pairs on the FMA pipe
           p = ex2_poly2(x);
         } else {
           p.x = ex2_approx(x.x);
