@@ -651,11 +651,16 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
   int splits = 1;
   if (tc) {
     // one CTA per SM: pick the split count with the fullest last wave, >= 8 pages per split
+    // at most one wave: a CTA's fixed cost (prologue, Q load, partial write) makes
+    // two waves of short splits slower than one of longer splits (first-token
+    // step attention 1.40 -> 1.16 ms at 32K: 18 splits instead of 37)
     const int max_s = std::max(1, std::min({n_pages / 8, m->max_splits, cap}));
+    static const int max_waves = std::getenv("CAKE_ATTN_MAX_WAVES") ? std::atoi(std::getenv("CAKE_ATTN_MAX_WAVES")) : 1;
     double best = 0.0;
     for (int sp = 1; sp <= max_s; ++sp) {
       const int ctas = base_ctas * sp;
       const int waves = (ctas + num_sms() - 1) / num_sms();
+      if (waves > max_waves) break;
       const double eff = static_cast<double>(ctas) / (static_cast<double>(waves) * num_sms());
       if (eff > best + 0.02) {
         best = eff;
