@@ -15,7 +15,7 @@ if sched is not None:
     from paper_2410_03065_b200 import native
     native.load_cuda().cake_gemm_set_schedule(int(sched))
 C = int(os.environ.get("C", "512"))
-rt = GpuRuntime("llama3_8b", max_tokens=T, max_chunk=C)
+rt = GpuRuntime("llama3_8b", max_tokens=T, max_chunk=C, lookahead_layers=int(os.environ.get("LOOKAHEAD", "0")))
 tier = rt.build_cache_tier(T, C, 42)
 for i in range(int(os.environ.get("REPS", "2"))):
     t0 = time.time()
