@@ -256,11 +256,21 @@ __global__ void __launch_bounds__(128) swiglu_tail_kernel(const GemmArgs a, int 
   }
   const int j = threadIdx.x;
   const float* src = a.tail_ws + (static_cast<size_t>(t) * parts * 256 + r) * 256;
+  // all parts' loads in flight at once (parts <= kTailSplit), then summed in part order
+  float gv[kTailSplit], uv[kTailSplit];
+#pragma unroll
+  for (int p = 0; p < kTailSplit; ++p)
+    if (p < parts) {
+      gv[p] = __ldcg(src + static_cast<size_t>(p) * 256 * 256 + j);
+      uv[p] = __ldcg(src + static_cast<size_t>(p) * 256 * 256 + 128 + j);
+    }
   float g = 0.f, u = 0.f;
-  for (int p = 0; p < parts; ++p) {
-    g += __ldcg(src + static_cast<size_t>(p) * 256 * 256 + j);
-    u += __ldcg(src + static_cast<size_t>(p) * 256 * 256 + 128 + j);
-  }
+#pragma unroll
+  for (int p = 0; p < kTailSplit; ++p)
+    if (p < parts) {
+      g += gv[p];
+      u += uv[p];
+    }
   __syncthreads();
   const float rs = s_rs;
   g *= rs;
