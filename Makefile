@@ -10,6 +10,10 @@ PKG     := paper_2410_03065_b200
 LIB     := $(PKG)/_lib
 INC     := -Iinclude
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden -Xptxas -v $(INC)
+# experiment-only attention kernels (two-tile, decoupled groups): make ATTN_VARIANTS=1
+ifeq ($(ATTN_VARIANTS),1)
+NVFLAGS += -DCAKE_ATTN_VARIANTS
+endif
 CXXFLAGS:= -O3 -std=c++20 -fPIC -Wall -Wextra -Wno-unused-parameter $(INC) -I/usr/local/cuda/include
 CUDA_LIBDIR := /usr/local/cuda/lib64
 

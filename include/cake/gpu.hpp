@@ -87,6 +87,7 @@ struct GpuRunInfo {
   std::uint64_t h2d_bytes = 0;
   std::uint64_t d2h_bytes = 0;
   std::vector<float> logits;
+  std::vector<SliceEvent> slices;  // RunOptions::record_slices
 };
 
 class GpuContext {
@@ -118,6 +119,9 @@ class GpuContext {
   std::vector<std::byte> read_chunk_kv(const ChunkSpec& chunk) const;
 
   const GpuRunInfo& last_run() const;
+  // Test instrumentation: fill the paged KV pool (both page sets) and the
+  // device staging buffers with `byte`, so stale bytes cannot pass a check.
+  void poison(int byte);
   TpCoordinator* tp() const;  // non-null for tp_size > 1 with a coordinator
 
   struct Impl;

@@ -76,6 +76,9 @@ typedef struct cake_run_opts {
   uint64_t jitter_seed;
   int race_to_finish; /* B200 extension */
   int cached_prefix;  /* B200 extension: the tier may hold only a leading run of chunks */
+  int record_slices;  /* log every released slice (TransferOptions::record_slices) */
+  int race_force;     /* test instrumentation (RunOptions::race_force): 0 policy, 1 compute contests, 2 io contests */
+  int race_hold;      /* test instrumentation (RunOptions::race_hold): -1 off, 0 compute waits, 1 io waits */
 } cake_run_opts;
 
 typedef struct cake_summary {
@@ -190,6 +193,14 @@ CAKE_API int cake_gpu_set_profiling(cake_gpu* g, int mask);
 CAKE_API int cake_gpu_set_profiling_stride(cake_gpu* g, int stride);
 /* 0 = tcgen05 attention (default), 1 = mma.sync attention (validation cross-check). */
 CAKE_API int cake_gpu_set_attention_impl(cake_gpu* g, int impl);
+/* Test instrumentation: fill the whole paged KV pool (spare page set
+ * included) and the device staging buffers with `byte` (0xFF = bf16 NaN), so
+ * a later run must write every page it references. */
+CAKE_API int cake_gpu_poison(cake_gpu* g, int byte);
+/* Slice log of the last run (record_slices): release time on the run clock
+ * and cumulative released bits (reference transfer.hpp SliceEvent). n_out = total. */
+CAKE_API int cake_gpu_slices(const cake_gpu* g, int64_t* at_us, uint64_t* cumulative_bits, uint64_t cap,
+                             uint64_t* n_out);
 CAKE_API void* cake_gpu_model(cake_gpu* g); /* cake_model* for direct C-ABI CUDA calls */
 CAKE_API void* cake_gpu_compute_stream(cake_gpu* g);
 

@@ -170,6 +170,9 @@ CAKE_API int cake_final_logits(cake_model* m, long long T, const int32_t* d_last
 /* Bytes of one chunk of chunk_len tokens in the cache-tier format
  * [layer][K|V][kv_head][token][head_dim] bf16 (this rank's shard). */
 CAKE_API long long cake_kv_chunk_bytes(const cake_model* m, int chunk_len);
+/* Test instrumentation: fill the whole paged pool (every physical page,
+ * spare set included) with `byte` on `stream` (0xFF = bf16 NaN). */
+CAKE_API int cake_kv_poison(cake_model* m, int byte, void* stream);
 /* staging bytes [byte_begin, byte_end) (16-B aligned) of a chunk starting at
  * token chunk_start -> paged pool through d_block_table. */
 CAKE_API int cake_kv_scatter(cake_model* m, const void* d_staging, long long chunk_start, int chunk_len,

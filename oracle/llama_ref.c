@@ -42,6 +42,24 @@ uint16_t ref_weight_bits(unsigned long long seed, uint32_t tensor_id, uint64_t l
   return ref_bf16_from_float(u * scale);
 }
 
+void ref_weight_matrix_bits(unsigned long long seed, uint32_t tid, long long rows, long long cols, float scale,
+                            uint16_t* out) {
+#pragma omp parallel for schedule(static)
+  for (long long r = 0; r < rows; ++r)
+    for (long long k = 0; k < cols; ++k)
+      out[r * cols + k] = ref_weight_bits(seed, tid, (uint64_t)(r * cols + k), scale);
+}
+
+void ref_weight_row_bits(unsigned long long seed, uint32_t tid, long long row, long long cols, float scale,
+                         uint16_t* out) {
+  for (long long k = 0; k < cols; ++k) out[k] = ref_weight_bits(seed, tid, (uint64_t)(row * cols + k), scale);
+}
+
+void ref_round_bf16(float* x, long long n) {
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < n; ++i) x[i] = round_bf16(x[i]);
+}
+
 enum { W_Q = 0, W_K = 1, W_V = 2, W_O = 3, W_GATE = 4, W_UP = 5, W_DOWN = 6 };
 #define TID_EMBED (1u << 20)
 #define TID_LMHEAD ((1u << 20) + 1u)

@@ -51,6 +51,15 @@ long long ref_max_tokens(const ref_model* m);
 
 /* Exact generator shared with the GPU (bf16 bits of one weight). */
 uint16_t ref_weight_bits(unsigned long long seed, uint32_t tensor_id, uint64_t logical_index, float scale);
+/* rows x cols block of tensor `tensor_id` (row-major, logical index r*cols+k) as bf16 bits,
+ * OpenMP-parallel — the weight source of the numpy oracle (oracle/llama_np.py). */
+void ref_weight_matrix_bits(unsigned long long seed, uint32_t tensor_id, long long rows, long long cols, float scale,
+                            uint16_t* out);
+/* Row `row` of a (*, cols) tensor: logical indices [row*cols, (row+1)*cols). */
+void ref_weight_row_bits(unsigned long long seed, uint32_t tensor_id, long long row, long long cols, float scale,
+                         uint16_t* out);
+/* bf16 rounding (nearest-even) of n floats in place. */
+void ref_round_bf16(float* x, long long n);
 uint16_t ref_bf16_from_float(float f);
 float ref_bf16_to_float(uint16_t b);
 

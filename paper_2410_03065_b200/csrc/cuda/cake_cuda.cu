@@ -18,8 +18,10 @@
 
 #include "attention.cuh"
 #include "attention_tc.cuh"
+#ifdef CAKE_ATTN_VARIANTS  // experiment kernels (A/B only): make ATTN_VARIANTS=1
 #include "attention_fa4.cuh"
 #include "attention_dec.cuh"
+#endif
 #include "cake_cuda.h"
 #include "elementwise.cuh"
 #include "gemm.cuh"
@@ -563,9 +565,10 @@ enum { kWq = 0, kWk = 1, kWv = 2, kWo = 3, kWgate = 4, kWup = 5, kWdown = 6 };
 
 namespace {
 
-constexpr long long kFa4MinPrefix = 1LL << 62;  // product never picks the two-tile kernel (see attention())
 long long* g_fa4_trace = nullptr;  // debug: clock stamps of one CTA (cake_debug_fa4_trace)
 int g_fa4_trace_layer = -1;
+
+#ifdef CAKE_ATTN_VARIANTS
 
 // Two-tile tcgen05 attention (attention_fa4.cuh): 2 x 128 (token, head) rows
 // of one KV head per CTA; splits of the prefix fill one wave of SMs, the last
@@ -631,14 +634,16 @@ int attention_fa4(cake_model* m, long long chunk_start, int chunk_len, int layer
   }
   return CAKE_OK;
 }
+#endif  // CAKE_ATTN_VARIANTS
 
 int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, const int32_t* bt,
               const int32_t* abort_flag, cudaStream_t s) {
   // Product dispatch (impl 0) is the one-tile kernel for every chunk: with
   // FFMA2/FADD2 softmax it is faster than the two-tile kernel at every prefix
   // measured (up to 32K, tools/attn_ab.py); impl 3 forces the two-tile kernel.
-  if ((m->attn_impl == 0 && chunk_start >= kFa4MinPrefix && chunk_len >= 128) || m->attn_impl == 3)
-    return attention_fa4(m, chunk_start, chunk_len, layer, bt, abort_flag, s);
+#ifdef CAKE_ATTN_VARIANTS
+  if (m->attn_impl == 3) return attention_fa4(m, chunk_start, chunk_len, layer, bt, abort_flag, s);
+#endif
   const int G = m->nq / m->nkv;
   const bool tc = m->attn_impl != 1;
   const int rows_per_cta = tc ? kFaRows : kAttnRows;
@@ -694,6 +699,7 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
     fa.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(m->hd));
     fa.abort_flag = abort_flag;
     fa.trace = (g_fa4_trace_layer == layer) ? g_fa4_trace : nullptr;
+#ifdef CAKE_ATTN_VARIANTS
     if (m->attn_impl == 4) {  // decoupled softmax groups (attention_dec.cuh)
       if (m->hd == 128) {
         auto kern = attn_dec_kernel<128>;
@@ -712,7 +718,9 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
         }
         CK(launch_chain(kern, grid, dim3(fa_threads<2>()), FdCfg<64>::kSmem, s, 1, m->tm_q, m->tm_kv, fa));
       }
-    } else if (m->hd == 128) {
+    } else
+#endif
+    if (m->hd == 128) {
       // two softmax groups (384 threads): four groups measured 10% slower at 32K (512-thread max exchange)
       auto kern = attn_tc_kernel<128, 2>;
       static bool cfgd = false;
@@ -1434,6 +1442,9 @@ CAKE_API int cake_debug_fa4_trace(void* dev_buf, int layer) {
 }
 
 int cake_model_set_attention_impl(cake_model* m, int impl) {
+#ifndef CAKE_ATTN_VARIANTS
+  if (impl == 3 || impl == 4) return fail(CAKE_EINVAL, "attention impl %d: built without ATTN_VARIANTS=1", impl);
+#endif
   if (impl < 0 || impl > 4)
     return fail(CAKE_EINVAL, "attention impl must be 0 (product dispatch), 1 (mma.sync), 2 (one-tile tcgen05), "
                              "3 (two-tile tcgen05) or 4 (one-tile, decoupled softmax groups)");
@@ -1587,6 +1598,12 @@ int cake_final_logits(cake_model* m, long long T, const int32_t* d_last_token, i
 
 long long cake_kv_chunk_bytes(const cake_model* m, int chunk_len) {
   return 2LL * m->L * m->nkv * m->hd * 2 * chunk_len;
+}
+
+int cake_kv_poison(cake_model* m, int byte, void* stream) {
+  if (!m) return fail(CAKE_EINVAL, "kv poison: null model");
+  CK(cudaMemsetAsync(m->pool, byte & 0xFF, m->pool_bytes, S(stream)));
+  return CAKE_OK;
 }
 
 static int kv_permute(cake_model* m, void* staging, long long chunk_start, int chunk_len, const int32_t* bt,

@@ -65,9 +65,12 @@ RunOptions to_opts(const cake_run_opts* o) {
   r.decode_us_per_byte = o->decode_us_per_byte;
   r.jitter_max_us = o->jitter_max_us;
   r.jitter_seed = o->jitter_seed;
+  r.record_slices = o->record_slices != 0;
 #ifndef CAKE_REFERENCE_BUILD
   r.race_to_finish = o->race_to_finish != 0;
   r.cached_prefix = o->cached_prefix != 0;
+  r.race_force = o->race_force;
+  r.race_hold = o->race_hold;
 #else
   if (o->race_to_finish) throw std::invalid_argument("race_to_finish is a B200 extension");
   if (o->cached_prefix) throw std::invalid_argument("cached_prefix is a B200 extension");
@@ -205,6 +208,9 @@ void cake_run_opts_default(cake_run_opts* o) {
   o->jitter_seed = d.jitter_seed;
   o->race_to_finish = 0;
   o->cached_prefix = 0;
+  o->record_slices = 0;
+  o->race_force = 0;
+  o->race_hold = -1;
 }
 
 int cake_sim_run(uint32_t n, const uint64_t* token_starts, const uint32_t* token_counts, const uint64_t* encoded_bytes,
@@ -510,6 +516,21 @@ int cake_gpu_set_profiling_stride(cake_gpu* g, int stride) {
 int cake_gpu_set_attention_impl(cake_gpu* g, int impl) {
   return guarded([&] {
     if (cake_model_set_attention_impl(g->ctx->model(), impl) != CAKE_OK) throw std::invalid_argument("bad impl");
+  });
+}
+
+int cake_gpu_poison(cake_gpu* g, int byte) {
+  return guarded([&] { g->ctx->poison(byte); });
+}
+
+int cake_gpu_slices(const cake_gpu* g, int64_t* at_us, uint64_t* cumulative_bits, uint64_t cap, uint64_t* n_out) {
+  return guarded([&] {
+    const auto& s = g->ctx->last_run().slices;
+    if (n_out) *n_out = s.size();
+    for (std::size_t i = 0; i < s.size() && i < cap; ++i) {
+      if (at_us) at_us[i] = s[i].at_us;
+      if (cumulative_bits) cumulative_bits[i] = s[i].cumulative_bits;
+    }
   });
 }
 

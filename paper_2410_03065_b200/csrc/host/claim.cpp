@@ -52,8 +52,17 @@ bool ClaimTable::all_claimed() const {
 
 std::optional<ClaimRecord> ClaimTable::record(std::uint32_t index) const {
   if (index >= n_) throw std::out_of_range("claim table: index out of range");
-  const std::uint64_t v = slots_[index].load(std::memory_order_acquire);
-  if (!(v & kTaken)) return std::nullopt;
+  // Taken-ness comes from the pointer word (the linearization point of a
+  // claim); the slot is stored right after the CAS, so a reader that sees the
+  // pointer past `index` waits out that window instead of reporting "free".
+  const std::uint64_t s = state_.load(std::memory_order_acquire);
+  if (!(index < lo(s) || static_cast<std::int64_t>(index) > io_ptr(s))) return std::nullopt;
+  std::uint64_t v;
+  while (!((v = slots_[index].load(std::memory_order_acquire)) & kTaken)) {
+#if defined(__x86_64__) || defined(__i386__)
+    __builtin_ia32_pause();
+#endif
+  }
   return ClaimRecord{(v & kIoBit) ? Side::io : Side::compute, static_cast<Micros>(v & kTimeMask)};
 }
 

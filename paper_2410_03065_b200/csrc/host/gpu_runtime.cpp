@@ -155,7 +155,7 @@ struct GpuContext::Impl {
   Pinned<float> h_logits;
   const std::int32_t* final_bt = nullptr;
   std::vector<std::unique_ptr<Event>> ev_start, ev_near, ev_end, ev_io;
-  std::unique_ptr<Event> ev_anchor, ev_copy_done, ev_final_start, ev_logits;  // created after set_device
+  std::unique_ptr<Event> ev_anchor, ev_copy_done, ev_final_start, ev_logits, ev_reset;  // created after set_device
   GpuRunInfo last;
   std::unique_ptr<TpCoordinator> tp;
   std::uint64_t run_counter = 0;
@@ -199,6 +199,7 @@ GpuContext::GpuContext(const GpuModelConfig& cfg, const GpuOptions& opt) : impl_
   g.ev_copy_done = std::make_unique<Event>();
   g.ev_final_start = std::make_unique<Event>();
   g.ev_logits = std::make_unique<Event>();
+  g.ev_reset = std::make_unique<Event>();
   check(cake_model_create(&mc, &g.model), "model create");
   check(cake_model_get_info(g.model, &g.info), "model info");
   // tp_size > 1 without a communicator is allowed for the single-device
@@ -380,6 +381,14 @@ CostModel GpuContext::calibrate(const RequestSpec& request, std::uint64_t prompt
   return cm;
 }
 
+void GpuContext::poison(int byte) {
+  Impl& g = *impl_;
+  check(cake_cuda_device_sync(), "poison: drain");
+  check(cake_kv_poison(g.model, byte, g.s_compute), "poison pool");
+  for (auto& s : g.staging) check(cake_memset_async(s.p, byte & 0xFF, g.staging_bytes, g.s_compute), "poison staging");
+  check(cake_stream_sync(g.s_compute), "poison: sync");
+}
+
 std::vector<std::byte> GpuContext::read_chunk_kv(const ChunkSpec& chunk) const {
   Impl& g = *impl_;
   const auto bytes = static_cast<std::size_t>(cake_kv_chunk_bytes(g.model, static_cast<int>(chunk.token_count)));
@@ -410,6 +419,7 @@ struct LiveRun {
   std::unique_ptr<std::atomic<int>[]> commit;
   std::atomic<int> race_chunk{-1};
   std::atomic<int> racer{-1};  // kByCompute / kByIo
+  int hold = kNone;            // RunOptions::race_hold: this side's commit of the contested chunk waits
   TransferEngine* loader = nullptr;
   TpCoordinator* tp = nullptr;  // leader side of a TP group (followers run run_follower)
   std::mutex commit_mu;
@@ -428,6 +438,14 @@ struct LiveRun {
   }
 
   bool try_commit(std::uint32_t i, int who) {
+    if (who == hold && race_chunk.load() == static_cast<int>(i)) {
+      // test instrumentation: let the other side win the contested chunk
+      const Micros deadline = timer.now_us() + 60'000'000;
+      while (commit[i].load() == kNone) {
+        if (timer.now_us() > deadline) throw std::runtime_error("race_hold: the other side never committed");
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+      }
+    }
     int expected = kNone;
     if (!commit[i].compare_exchange_strong(expected, who)) return false;
     {
@@ -449,11 +467,21 @@ struct LiveRun {
     }
   }
 
-  // Second page set for contested chunk k, uploaded on the racer's stream
-  // ahead of the racer's writes.
-  void start_race(const ChunkSpec& c, int who, void* stream) {
-    race_chunk.store(static_cast<int>(c.index));
+  // One contested chunk per run: the side whose contest predicate fires
+  // first takes the race slot (the spare page set and h_bt_race are single).
+  bool reserve_race(std::uint32_t i, int who) {
+    int expected = -1;
+    if (!race_chunk.compare_exchange_strong(expected, -2)) return false;  // -2: being set up
     racer.store(who);
+    race_chunk.store(static_cast<int>(i));
+    return true;
+  }
+
+  // Second page set for the reserved contested chunk, uploaded on the
+  // racer's stream ahead of the racer's writes.
+  void start_race(const ChunkSpec& c, int who, void* stream) {
+    if (race_chunk.load() != static_cast<int>(c.index) || racer.load() != who)
+      throw std::logic_error("race: chunk contested without the race slot");
     const int first = static_cast<int>(c.token_start / g.cfg.page_tokens);
     for (int p = 0; p < g.n_pages; ++p) g.h_bt_race.p[p] = p;
     for (int p = 0; p < g.pages_of(c); ++p) g.h_bt_race.p[first + p] = g.n_pages + p;
@@ -530,6 +558,8 @@ class GpuPrefillBackend final : public PrefillBackend {
   int last_launched() const { return last_launched_; }
 
  private:
+  // Callers on the loader thread hold mu_; the compute thread (the only
+  // writer of launched_ and of the ratio, both under mu_) may read unlocked.
   Micros duration(const ChunkSpec& c) const {
     const double base = static_cast<double>(compute_latency(prior_, c, 1.0));
     const double ratio = den_ > 0 ? num_ / den_ : 1.0;
@@ -549,6 +579,7 @@ class GpuPrefillBackend final : public PrefillBackend {
       if (cake_event_query(r_.g.ev_end[i]->h) != CAKE_OK) break;
       float ms = 0.f;
       check(cake_event_elapsed_ms(r_.g.ev_start[i]->h, r_.g.ev_end[i]->h, &ms), "elapsed");
+      std::lock_guard lk(mu_);
       num_ += static_cast<double>(ms) * 1000.0;
       den_ += static_cast<double>(compute_latency(prior_, r_.plan.chunks[i], 1.0));
       ++observed_;
@@ -770,8 +801,12 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   run.tp = tp;
   check(cake_event_record(g.ev_anchor->h, g.s_compute), "anchor");
   run.t0 = timer.now_us();
+  run.hold = opt.race_hold == 0 ? kByCompute : opt.race_hold == 1 ? kByIo : kNone;
   check(cake_stream_wait_event(g.s_copy, g.ev_anchor->h), "order");
   check(cake_memset_async(g.abort_flags.p, 0, g.n_pages * sizeof(std::int32_t), g.s_compute), "abort reset");
+  // abort writes go on the control stream: order them after the reset
+  check(cake_event_record(g.ev_reset->h, g.s_compute), "record");
+  check(cake_stream_wait_event(g.s_control, g.ev_reset->h), "order");
   upload_tokens(g, tokens, g.s_compute);
   GpuRunInfo info;
   info.h2d_bytes = tokens.size() * sizeof(std::int32_t);
@@ -789,8 +824,13 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
     t.sink = &sink;
     if (race) {
       t.contest = [&](const FetchTask& task, Micros io_eta) {
-        const auto c_eta = backend.expected_end_of(task.chunk.index);
-        return c_eta && io_eta + g.opt.race_margin_us < *c_eta;
+        if (opt.race_force == 1) return false;
+        bool want = opt.race_force == 2;
+        if (!want) {
+          const auto c_eta = backend.expected_end_of(task.chunk.index);
+          want = c_eta && io_eta + g.opt.race_margin_us < *c_eta;
+        }
+        return want && run.reserve_race(task.chunk.index, kByIo);
       };
     }
     loader = std::make_unique<TransferEngine>(store, trace, codec, &table, timer, std::move(t));
@@ -818,8 +858,11 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
     }
     if (race) {
       hooks.contest = [&](const ChunkSpec& c, Micros c_eta) {
+        if (opt.race_force == 2) return false;
         const auto io_eta = loader->inflight_finish_estimate(c.index);
-        return io_eta && c_eta + g.opt.race_margin_us < *io_eta;
+        if (!io_eta) return false;  // nothing in flight to race
+        const bool want = opt.race_force == 1 || c_eta + g.opt.race_margin_us < *io_eta;
+        return want && run.reserve_race(c.index, kByCompute);
       };
     }
     auto recs = engine.run_forward(plan.chunks, plan.keys, hooks);
@@ -873,6 +916,7 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   if (loader) {
     loader->wait();
     rep.chunks.insert(rep.chunks.end(), loader->records().begin(), loader->records().end());
+    info.slices = loader->slices();
   }
   for (const ChunkSpec& c : plan.suffix)
     rep.chunks.push_back({c.index, Side::compute, run.device_time(g.ev_start[c.index]->h),

@@ -32,7 +32,8 @@ class CakeRecord(C.Structure):
 class CakeRunOpts(C.Structure):
     _fields_ = [("compute_enabled", C.c_int), ("io_enabled", C.c_int), ("token_budget", u32),
                 ("throttle_quantum_bytes", u64), ("decode_us_per_byte", dbl), ("jitter_max_us", u32),
-                ("jitter_seed", u64), ("race_to_finish", C.c_int), ("cached_prefix", C.c_int)]
+                ("jitter_seed", u64), ("race_to_finish", C.c_int), ("cached_prefix", C.c_int),
+                ("record_slices", C.c_int), ("race_force", C.c_int), ("race_hold", C.c_int)]
 
 
 class CakeSummary(C.Structure):
@@ -107,6 +108,8 @@ _SIGS = {
     "cake_gpu_set_profiling": (C.c_int, [vp, C.c_int]),
     "cake_gpu_set_profiling_stride": (C.c_int, [vp, C.c_int]),
     "cake_gpu_set_attention_impl": (C.c_int, [vp, C.c_int]),
+    "cake_gpu_poison": (C.c_int, [vp, C.c_int]),
+    "cake_gpu_slices": (C.c_int, [vp, P(i64), P(u64), u64, P(u64)]),
     "cake_gpu_model": (vp, [vp]),
     "cake_gpu_compute_stream": (vp, [vp]),
     "cake_tp_create": (C.c_int, [C.c_char_p, C.c_int, C.c_int, P(vp)]),

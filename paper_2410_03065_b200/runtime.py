@@ -127,6 +127,24 @@ class GpuRuntime:
         self.n.call("cake_gpu_logits", self.h, out.ctypes.data, self.vocab)
         return out
 
+    def poison(self, byte: int = 0xFF):
+        """Test instrumentation: fill the paged KV pool (both page sets) and the
+        device staging buffers with `byte` (0xFF = bf16 NaN) so a later run must
+        write every page its block table references."""
+        self.n.call("cake_gpu_poison", self.h, byte)
+
+    def slices(self) -> tuple[np.ndarray, np.ndarray]:
+        """Slice log of the last run (record_slices=True): (release time on the
+        run clock in us, cumulative released bits) — reference transfer.hpp SliceEvent."""
+        n = N.u64()
+        self.n.call("cake_gpu_slices", self.h, None, None, 0, C.byref(n))
+        at = np.zeros(n.value, dtype=np.int64)
+        bits = np.zeros(n.value, dtype=np.uint64)
+        if n.value:
+            self.n.call("cake_gpu_slices", self.h, at.ctypes.data_as(C.POINTER(N.i64)),
+                        bits.ctypes.data_as(C.POINTER(N.u64)), n.value, C.byref(n))
+        return at, bits
+
     def read_chunk(self, token_start: int, token_count: int) -> bytes:
         L, H, nh, nkv, hd, ffn, vocab = self.dims
         nbytes = self.kv_bytes_per_token * token_count

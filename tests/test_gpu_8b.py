@@ -1,6 +1,7 @@
 """Llama-3-8B shape on the B200.
 
-* reduced depth (2 of 32 layers), T=1024: KV + first-token logits vs the CPU oracle;
+(oracle parity at this shape: tests/test_gpu_depth.py)
+
 * full depth, BASELINE config sizes (32K context): size-independent properties —
   every loaded chunk bit-exact vs the cache tier, the assembled cache bit-identical
   to the compute-only cache wherever the merge point lands, exactly-once coverage,
@@ -14,50 +15,12 @@ pytestmark = pytest.mark.gpu
 DIMS = (32, 4096, 32, 8, 128, 14336, 128256)
 
 
-def top1_ok(got, want, tol=2e-2):
-    """GPU arg-max is the oracle's arg-max, or a near-tie within the stated tolerance."""
-    return want[int(got.argmax())] >= want.max() - tol * np.abs(want).max()
-
-
-def rel(a, b):
-    return float(np.abs(a - b).max() / (np.abs(b).max() + 1e-12))
-
-
 @pytest.fixture(scope="module")
 def gpu():
     import torch
 
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
-
-
-@pytest.mark.parametrize("impl", ["tcgen05", "tcgen05_2tile", "tcgen05_dec"])
-def test_8b_two_layers_vs_oracle(gpu, impl):
-    """Product dispatch, and the two-tile attention kernel forced for every chunk."""
-    import llama_oracle
-    from paper_2410_03065_b200.cake import Cake
-    from paper_2410_03065_b200.runtime import GpuRuntime
-
-    T, C, seed = 1024, 512, 7
-    rt = GpuRuntime("llama3_8b", n_layers=2, max_tokens=T, max_chunk=C)
-    rt.set_attention_impl(impl)
-    tier = rt.build_cache_tier(T, C, seed)
-    dims = (2,) + DIMS[1:]
-    toks = Cake().token_stream(seed, T).astype(np.int32)
-    ref = llama_oracle.LlamaRef(dims, T, cache_weight_bytes=8 << 30)
-    for s in range(0, T, C):
-        ref.prefill_chunk(toks[s:s + C], s)
-    want = ref.final_logits(C - 1)
-    rt.run(tier, T, C, seed, mbps=64000, mode="compute_only")
-    lg = rt.logits()
-    assert rel(lg, want) <= 2e-2 and top1_ok(lg, want)
-    kv = ref.kv()
-    for s in range(0, T, C):
-        got = llama_oracle.bf16_to_f32(np.frombuffer(rt.read_chunk(s, C), dtype=np.uint16)).reshape(2, 2, 8, C, 128)
-        assert rel(got, kv[:, :, :, s:s + C, :]) <= 2e-2
-    rt.run(tier, T, C, seed, mbps=64000, mode="io_only")  # loaded tail -> recomputed last token
-    lg2 = rt.logits()
-    assert rel(lg2, want) <= 2e-2 and top1_ok(lg2, want)
 
 
 def test_8b_full_32k_properties(gpu):
@@ -69,6 +32,7 @@ def test_8b_full_32k_properties(gpu):
     rt.calibrate(T, C, seed)
     tier = rt.build_cache_tier(T, C, seed)
     n = T // C
+    rt.poison(0xFF)
     c_only = rt.run(tier, T, C, seed, mbps=64000, mode="compute_only")
     sample = sorted({0, 1, n // 2, n - 2, n - 1})
     base = {i: rt.read_chunk(i * C, C) for i in sample}
@@ -81,11 +45,12 @@ def test_8b_full_32k_properties(gpu):
         assert base[i] == tier.get(keys[i])
     for mbps in (16000, 64000, 256000):
         io_only = rt.run(tier, T, C, seed, mbps=mbps, mode="io_only")
+        rt.poison(0xFF)
         r = rt.run(tier, T, C, seed, mbps=mbps, mode="cake")
         assert sorted(c.index for c in r.chunks) == list(range(n))
         assert all((c.side == "compute") == (c.index < r.merge_point) for c in r.chunks)
-        for i in sample:
-            assert rt.read_chunk(i * C, C) == base[i], (mbps, i, r.merge_point)
+        for i in range(n):  # from a poisoned pool: every chunk landed or computed in this run
+            assert rt.read_chunk(i * C, C) == (base[i] if i in base else tier.get(keys[i])), (mbps, i, r.merge_point)
         # bidirectional never loses to the better single-sided mode (small slack for device jitter)
         assert r.device_ttft_ms <= min(c_only.device_ttft_ms, io_only.device_ttft_ms) * 1.03 + 1.0, \
             (mbps, r.device_ttft_ms, c_only.device_ttft_ms, io_only.device_ttft_ms)
