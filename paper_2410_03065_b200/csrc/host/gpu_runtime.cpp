@@ -420,6 +420,7 @@ struct LiveRun {
   std::atomic<int> race_chunk{-1};
   std::atomic<int> racer{-1};  // kByCompute / kByIo
   int hold = kNone;            // RunOptions::race_hold: this side's commit of the contested chunk waits
+  std::atomic<bool> compute_done{false};  // the compute side claims nothing more
   TransferEngine* loader = nullptr;
   TpCoordinator* tp = nullptr;  // leader side of a TP group (followers run run_follower)
   std::mutex commit_mu;
@@ -438,13 +439,21 @@ struct LiveRun {
   }
 
   bool try_commit(std::uint32_t i, int who) {
-    if (who == hold && race_chunk.load() == static_cast<int>(i)) {
-      // test instrumentation: let the other side win the contested chunk
+    if (who == hold) {
+      // test instrumentation: the held side commits nothing until the other
+      // side has decided whether to contest, and lets it win a contested chunk
       const Micros deadline = timer.now_us() + 60'000'000;
-      while (commit[i].load() == kNone) {
-        if (timer.now_us() > deadline) throw std::runtime_error("race_hold: the other side never committed");
-        std::this_thread::sleep_for(std::chrono::microseconds(50));
-      }
+      auto wait_for = [&](auto&& done) {
+        while (!done()) {
+          if (timer.now_us() > deadline) throw std::runtime_error("race_hold: the other side never decided");
+          std::this_thread::sleep_for(std::chrono::microseconds(50));
+        }
+      };
+      wait_for([&] {
+        if (race_chunk.load() >= 0) return true;
+        return who == kByCompute ? (loader == nullptr || loader->reader_finished()) : compute_done.load();
+      });
+      if (race_chunk.load() == static_cast<int>(i)) wait_for([&] { return commit[i].load() != kNone; });
     }
     int expected = kNone;
     if (!commit[i].compare_exchange_strong(expected, who)) return false;
@@ -801,7 +810,7 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   run.tp = tp;
   check(cake_event_record(g.ev_anchor->h, g.s_compute), "anchor");
   run.t0 = timer.now_us();
-  run.hold = opt.race_hold == 0 ? kByCompute : opt.race_hold == 1 ? kByIo : kNone;
+  run.hold = !race ? kNone : opt.race_hold == 0 ? kByCompute : opt.race_hold == 1 ? kByIo : kNone;
   check(cake_stream_wait_event(g.s_copy, g.ev_anchor->h), "order");
   check(cake_memset_async(g.abort_flags.p, 0, g.n_pages * sizeof(std::int32_t), g.s_compute), "abort reset");
   // abort writes go on the control stream: order them after the reset
@@ -854,7 +863,14 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
     hooks.backend = &backend;
     if (loader) {
       hooks.probe = &loader->resident_set();
-      hooks.signal_stop = [&loader] { loader->stop(); };
+      // race_force 2 (test): the loader goes on to its failing claim (and contests it) instead of
+      // being stopped when the compute side runs out of chunks
+      hooks.signal_stop = [&] {
+        run.compute_done.store(true);
+        if (opt.race_force != 2) loader->stop();
+      };
+    } else {
+      hooks.signal_stop = [&] { run.compute_done.store(true); };
     }
     if (race) {
       hooks.contest = [&](const ChunkSpec& c, Micros c_eta) {
