@@ -26,6 +26,7 @@
 #include "elementwise.cuh"
 #include "gemm.cuh"
 #include "gemm2.cuh"
+#include "gemm2c.cuh"
 #include "skinny.cuh"
 
 using namespace cake_dev;
@@ -139,6 +140,21 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uin
   return CAKE_OK;
 }
 
+// Row-major fp32 [rows, cols] with a (32 x box_rows) SW128 box (128-B rows).
+int make_map_f32(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(CAKE_ESTATE, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t elem[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, elem,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CAKE_EINVAL, "fp32 tensor map encode failed (%d)", (int)r);
+  return CAKE_OK;
+}
+
 // bf16 3-D tensor [d2][d1][d0] (d0 contiguous), SW128, box (64, b1, b2).
 int make_map_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b1, uint32_t b2) {
   auto fn = encode_fn();
@@ -181,6 +197,8 @@ int g_gemm_2sm = 1;       // 1: M > 128 projections use the 2-SM (cta_group::2) 
 int g_gemm_2sm_n128 = 1;  // O / down (N tiles of 128) on CTA pairs: down 59.9 -> 54.0 us at M = 512
 int g_gemm_hints = 3;     // L2 policy of the operand loads (GemmArgs::l2_hints)
 int g_gemm_tail_split = 1;  // gate/up: split the short last round along K (swiglu_tail_kernel)
+int g_gemm_prefetch = -1;   // gemm2c: weight k-blocks requested before the PDL wait (-1 whole ring)
+int g_gemm_pairs = 2;       // > 1: N-128/192 projections in clusters of this many CTA pairs sharing A (gemm2c)
 int g_gemm_qkv192 = 1;      // QKV on CTA-pair tiles of N 192 (rope-unit weight rows) when the rows tile
 
 // Tail-split partials of whole_tiles == 2 launches (stream-ordered reuse).
@@ -351,9 +369,85 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
   return CAKE_OK;
 }
 
-int gemm_dispatch(int bn, int epi, const CUtensorMap& ta, const CUtensorMap* tb3, const GemmArgs& a_in,
+// 2-SM GEMM in clusters of NP pairs sharing the A k-block (gemm2c.cuh): one
+// tile (m-pair x NP n-blocks) per cluster per round, no split. ta_piece is the
+// A map with 128 / NP-row boxes.
+template <int BLOCK_N, int EPI, int NP>
+int launch_gemm2c(const CUtensorMap& ta_piece, const CUtensorMap& tb_half, const CUtensorMap* om, GemmArgs a,
                   cudaStream_t s) {
+  using Cfg = Gemm2Cfg<BLOCK_N>;
+  auto kern = gemm2c_tc_kernel<BLOCK_N, EPI, NP>;
+  static bool configured = false;
+  static int max_clusters = 0, for_sms = 0;
+  if (!configured) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes));
+    if (NP * 2 > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  if (for_sms != num_sms()) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2 * NP;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(2 * NP * 16);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = num_sms() / (2 * NP);
+    }
+    max_clusters = std::min(n, num_sms() / (2 * NP));
+    for_sms = num_sms();
+  }
+  a.num_m_blocks = (a.M + kGemmBlockM - 1) / kGemmBlockM;
+  a.num_n_blocks = a.N / BLOCK_N;
+  a.num_k_blocks = a.K / kGemmBlockK;
+  a.cs = 2 * NP;
+  a.whole_tiles = 1;
+  const int tiles = ((a.num_m_blocks + 1) / 2) * (a.num_n_blocks / NP);
+  const int clusters = std::max(1, std::min(tiles, max_clusters));
+  // output maps (h fp32, bf16(h)): the staged residual epilogue, one tile per CTA
+  a.prefetch = g_gemm_prefetch;
+  a.staged = (EPI == kEpiResid && BLOCK_N == 128 && om != nullptr && tiles <= clusters) ? 1 : 0;
+  const CUtensorMap& th = a.staged ? om[0] : ta_piece;
+  const CUtensorMap& tx = a.staged ? om[1] : ta_piece;
+  CK(launch_chain(kern, dim3(2 * NP * clusters), dim3(kGemmThreads), Cfg::kSmemBytes, s, 2 * NP, ta_piece, tb_half,
+                  th, tx, a));
+  return CAKE_OK;
+}
+
+// Whether the cluster kernel takes this projection: N-128/192 pair tiles whose
+// n-blocks group by NP and whose cluster tiles fit one round of the GPU.
+bool use_gemm2c(int bn, int M, int N, int np) {
+  if (np <= 1 || M <= kGemmBlockM || (bn != 128 && bn != 192) || N % bn) return false;
+  const int nb = N / bn;
+  if (nb % np) return false;
+  const int tiles = ((M + 255) / 256) * (nb / np);
+  return tiles <= num_sms() / (2 * np);
+}
+
+template <int BLOCK_N, int EPI>
+int launch_gemm2c_np(const CUtensorMap* ta3, const CUtensorMap& tb_half, const CUtensorMap* om, const GemmArgs& a,
+                     cudaStream_t s) {
+  if (g_gemm_pairs == 4) return launch_gemm2c<BLOCK_N, EPI, 4>(ta3[2], tb_half, om, a, s);
+  return launch_gemm2c<BLOCK_N, EPI, 2>(ta3[1], tb_half, om, a, s);
+}
+
+long long* g_gemm_trace = nullptr;  // debug: per-launch stamp slots (cake_gemm_debug_trace)
+int g_gemm_trace_n = 0, g_gemm_trace_cap = 0;
+
+// om: optional output maps of a residual projection ([0] h fp32 32-col boxes,
+// [1] bf16(h) 64-col boxes, 128 rows each) for the staged epilogue.
+int gemm_dispatch(int bn, int epi, const CUtensorMap* ta3, const CUtensorMap* tb3, const GemmArgs& a_in,
+                  cudaStream_t s, const CUtensorMap* om = nullptr) {
+  const CUtensorMap& ta = ta3[0];
   GemmArgs a = a_in;
+  if (g_gemm_trace != nullptr && g_gemm_trace_n < g_gemm_trace_cap) a.trace = g_gemm_trace + 32LL * g_gemm_trace_n++;
   a.l2_hints = g_gemm_hints;
   // Chunks of more than 128 rows run on CTA pairs (cta_group::2): the pair's
   // MMA is M = 256 x N = bn, each CTA receiving its 128 rows of A and bn/2 rows
@@ -362,6 +456,21 @@ int gemm_dispatch(int bn, int epi, const CUtensorMap& ta, const CUtensorMap* tb3
   // At M = 512: QKV / gate-up 48 / 224 pair tiles of N 256, O / down 64 pair
   // tiles of N 128 (down 54.0 us against 59.9 on 1-SM 128 x 128 tiles, O 20.8
   // against 21.6; schedule bit 8 restores the 1-SM tiles).
+  if (g_gemm_2sm && use_gemm2c(bn, a.M, a.N, g_gemm_pairs)) {
+    // B maps: index 1 holds bn/2-row boxes (the pair kernels' weight halves)
+    if (bn == 192) {
+      switch (epi) {
+        case kEpiBf16: return launch_gemm2c_np<192, kEpiBf16>(ta3, tb3[1], nullptr, a, s);
+        case kEpiQkv: return launch_gemm2c_np<192, kEpiQkv>(ta3, tb3[1], nullptr, a, s);
+      }
+    } else {
+      switch (epi) {
+        case kEpiBf16: return launch_gemm2c_np<128, kEpiBf16>(ta3, tb3[1], nullptr, a, s);
+        case kEpiF32: return launch_gemm2c_np<128, kEpiF32>(ta3, tb3[1], nullptr, a, s);
+        case kEpiResid: return launch_gemm2c_np<128, kEpiResid>(ta3, tb3[1], om, a, s);
+      }
+    }
+  }
   if (bn == 192) {
     if (a.M <= kGemmBlockM || a.N % bn) return fail(CAKE_EINVAL, "gemm: N-192 tiles need M > 128 and N %% 192 == 0");
     switch (epi) {
@@ -466,7 +575,8 @@ struct cake_model {
   float* tp_buf = nullptr;  // fp32 partial sums for the TP all-reduce
   float* ss = nullptr;      // fused RMSNorm: [H / 128][rows_cap] partial sums of squares of the residual rows
   unsigned* q8_ws = nullptr;  // quant8 encode: ordered min/max keys
-  CUtensorMap a_xn, a_attn, a_act;
+  CUtensorMap a_xn[3], a_attn[3], a_act[3];
+  CUtensorMap out_h[2];  // staged residual epilogue: h (fp32, 32-col boxes), xn = bf16(h) (64-col boxes)  // activation maps, boxes of 128 / 64 / 32 rows (gemm2c pieces)
   CUtensorMap tm_q, tm_kv;  // attention: Q rows of a GQA group, paged K/V pool
   int attn_impl = 0;        // 0 product dispatch, 1 mma.sync (cross-check), 2 one-tile / 3 two-tile tcgen05 only
   int* attn_tickets = nullptr;  // split arrival tickets of the two-tile kernel (zero at rest)
@@ -918,7 +1028,7 @@ int rmsnorm(cake_model* m, const bf16* gamma, long long row0, int rows, const in
 }
 
 // Row-parallel projection output: residual += acc (TP: via all-reduce of partials).
-int row_parallel(cake_model* m, int kind, const CUtensorMap& ta, const CUtensorMap* tb, int K, int M,
+int row_parallel(cake_model* m, int kind, const CUtensorMap* ta, const CUtensorMap* tb, int K, int M,
                  const int32_t* abort_flag, cudaStream_t s) {
   GemmArgs g{};
   g.M = M;
@@ -936,7 +1046,7 @@ int row_parallel(cake_model* m, int kind, const CUtensorMap& ta, const CUtensorM
       g.ss_ld = m->rows_cap;
     }
     ProfScope ps(m, kind, s, flops, bytes);
-    return gemm_dispatch(128, kEpiResid, ta, tb, g, s);
+    return gemm_dispatch(128, kEpiResid, ta, tb, g, s, g.xb_out != nullptr ? m->out_h : nullptr);
   }
   if (!m->comm && !m->emulated_tp) return fail(CAKE_ESTATE, "tp_size > 1 but no NCCL communicator attached");
   g.out = m->tp_buf;
@@ -1377,9 +1487,13 @@ int cake_model_create(const cake_model_config* cfg, cake_model** out) {
   cudaMemset(m->xn, 0, R * H * sizeof(bf16));
   cudaMemset(m->attn, 0, R * m->nq * hd * sizeof(bf16));
   cudaMemset(m->act, 0, R * F * sizeof(bf16));
-  if ((st = make_map(&m->a_xn, m->xn, R, H, 128))) return bail(st);
-  if ((st = make_map(&m->a_attn, m->attn, R, m->nq * hd, 128))) return bail(st);
-  if ((st = make_map(&m->a_act, m->act, R, F, 128))) return bail(st);
+  if ((st = make_map_f32(&m->out_h[0], m->h, R, H, H, 128))) return bail(st);
+  if ((st = make_map(&m->out_h[1], m->xn, R, H, 128))) return bail(st);
+  for (int i = 0; i < 3; ++i) {
+    if ((st = make_map(&m->a_xn[i], m->xn, R, H, 128 >> i))) return bail(st);
+    if ((st = make_map(&m->a_attn[i], m->attn, R, m->nq * hd, 128 >> i))) return bail(st);
+    if ((st = make_map(&m->a_act[i], m->act, R, F, 128 >> i))) return bail(st);
+  }
   {
     const int G = m->nq / m->nkv;
     if ((st = make_map_3d(&m->tm_q, m->q, hd, m->nq, R, G, kFaRows / G))) return bail(st);
@@ -1678,8 +1792,12 @@ int cake_kv_encode_q8(cake_model* m, const void* d_chunk, int chunk_len, void* d
 
 int cake_gemm_set_schedule(int schedule) {
   // bit 0: stream-K; bit 1: disable the 2-SM kernel; bit 2: 1-SM weight multicast clusters
-  if (schedule < 0 || schedule > 255)
-    return fail(CAKE_EINVAL, "schedule bits: 1 stream-K, 2 no-2SM, 4 multicast, 8 1-SM N-128 tiles, 128 no QKV N-192");
+  g_gemm_prefetch = ((schedule >> 10) & 15) - 1;  // bits 10-13: 1 + weight stages prefetched before the PDL wait
+  schedule &= 1023;
+  if (schedule < 0)
+    return fail(CAKE_EINVAL, "schedule bits: 1 stream-K, 2 no-2SM, 4 multicast, 8 1-SM N-128 tiles, 128 no QKV N-192, "
+                             "256 no A-sharing pair clusters, 512 four pairs per cluster");
+  g_gemm_pairs = (schedule & 256) ? 1 : (schedule & 512) ? 4 : 2;
   g_gemm_qkv192 = (schedule & 128) ? 0 : 1;
   g_gemm_2sm_n128 = (schedule & 8) ? 0 : 1;
   g_gemm_hints = 3 ^ ((schedule >> 4) & 3);  // bits 4/5 drop the evict_last hint of A / B
@@ -1690,11 +1808,21 @@ int cake_gemm_set_schedule(int schedule) {
   return CAKE_OK;
 }
 
+// Debug: stamp %globaltimer at fixed points of the first / last CTA of the
+// next `cap` pair-cluster GEMM launches into dev_buf[32 * launch + slot]; nullptr stops.
+CAKE_API int cake_gemm_debug_trace(long long* dev_buf, int cap) {
+  g_gemm_trace = dev_buf;
+  g_gemm_trace_n = 0;
+  g_gemm_trace_cap = cap;
+  return CAKE_OK;
+}
+
 int cake_gemm(const void* dA, const void* dB, void* dC, int M, int N, int K, int epi, int block_n, void* stream) {
   if (M < 1 || N < 1 || K < 64 || K % 64 || N % block_n) return fail(CAKE_EINVAL, "gemm: bad shape");
   if (epi < 0 || epi > 2) return fail(CAKE_EINVAL, "gemm: epi must be 0..2");
-  CUtensorMap ta, tb[3];
-  CKS(make_map(&ta, dA, static_cast<uint64_t>(M), static_cast<uint64_t>(K), 128));
+  CUtensorMap ta[3], tb[3];
+  for (int i = 0; i < 3; ++i)
+    CKS(make_map(&ta[i], dA, static_cast<uint64_t>(M), static_cast<uint64_t>(K), static_cast<uint32_t>(128 >> i)));
   for (int ci = 0; ci < 3; ++ci)
     CKS(make_map(&tb[ci], dB, static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint32_t>(block_n >> ci)));
   GemmArgs g{};
@@ -1705,7 +1833,12 @@ int cake_gemm(const void* dA, const void* dB, void* dC, int M, int N, int K, int
   g.ldo = N;
   g.resid = static_cast<float*>(dC);
   g.ldr = N;
-  return gemm_dispatch(block_n, epi, ta, tb, g, S(stream));
+  CUtensorMap om[2];
+  if (epi == 2) {
+    CKS(make_map_f32(&om[0], dC, static_cast<uint64_t>(M), static_cast<uint64_t>(N), static_cast<uint64_t>(N), 128));
+    om[1] = om[0];  // no bf16 copy (xb_out == nullptr)
+  }
+  return gemm_dispatch(block_n, epi, ta, tb, g, S(stream), epi == 2 ? om : nullptr);
 }
 
 }  // extern "C"

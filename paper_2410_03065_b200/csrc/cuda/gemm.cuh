@@ -84,7 +84,23 @@ struct GemmArgs {
   int ss_parts, ss_ld, rms_dim;
   float rms_eps;
   int l2_hints;             // experiment: bit 0 A evict_last, bit 1 B evict_last (else evict_normal)
+  long long* trace;         // debug (cake_gemm_debug_trace): %globaltimer stamps of the first and last CTA
+  int staged;               // gemm2c kEpiResid: stage h / bf16(h) in shared memory, TMA-store them (1 tile per CTA)
+  int prefetch;             // gemm2c: weight k-blocks requested before the PDL wait (-1: the whole ring)
 };
+
+__device__ __forceinline__ long long globaltimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Stamp slot i of the launch's trace (first CTA: slots 0..15, last CTA: 16..31).
+__device__ __forceinline__ void gemm_stamp(const GemmArgs& a, int i) {
+  if (a.trace == nullptr) return;
+  if (blockIdx.x == 0) a.trace[i] = globaltimer_ns();
+  else if (blockIdx.x == gridDim.x - 1) a.trace[16 + i] = globaltimer_ns();
+}
 
 __device__ __forceinline__ uint64_t gemm_policy(int hints, int bit) {
   return (hints >> bit) & 1 ? policy_evict_last() : policy_evict_normal();

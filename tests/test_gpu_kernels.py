@@ -61,6 +61,36 @@ def test_gemm_matches_torch(cu, M, N, K, bn, epi):
     assert (got - ref).abs().max().item() <= tol
 
 
+@pytest.mark.parametrize("M,N,K,bn", [(512, 4096, 4096, 128), (512, 6144, 4096, 192), (384, 4096, 14336, 128),
+                                      (1024, 4096, 1024, 128), (200, 1024, 512, 128)])
+@pytest.mark.parametrize("schedule", [0, 256, 512])
+def test_gemm_pair_clusters_match_torch(cu, M, N, K, bn, schedule):
+    """Schedule 0: the A-sharing pair clusters (gemm2c, 2 pairs), 512: 4 pairs,
+    256: unclustered pairs (gemm2) — against torch, every epilogue."""
+    import torch
+
+    assert cu.cake_gemm_set_schedule(schedule) == 0
+    try:
+        for epi in (0, 1, 2):
+            if bn == 192 and epi != 0:
+                continue
+            g = torch.Generator(device="cuda").manual_seed(M + N + K + epi)
+            a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+            b = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
+            ref = a.float() @ b.float().t()
+            c = (torch.empty(M, N, device="cuda", dtype=torch.bfloat16) if epi == 0 else
+                 torch.full((M, N), 0.5, device="cuda", dtype=torch.float32))
+            st = cu.cake_gemm(a.data_ptr(), b.data_ptr(), c.data_ptr(), M, N, K, epi, bn, _stream())
+            assert st == 0, _err(cu)
+            torch.cuda.synchronize()
+            got = c.float() - (0.5 if epi == 2 else 0.0)
+            scale = ref.abs().max().item()
+            tol = 1e-2 * scale if epi == 0 else 2e-4 * scale
+            assert (got - ref).abs().max().item() <= tol, (epi, (got - ref).abs().max().item())
+    finally:
+        cu.cake_gemm_set_schedule(0)
+
+
 def test_gemm_rejects_bad_shapes(cu):
     st = cu.cake_gemm(None, None, None, 128, 100, 64, 0, 128, None)
     assert st != 0 and "bad shape" in _err(cu)
