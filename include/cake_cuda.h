@@ -227,6 +227,13 @@ CAKE_API int cake_model_launch_count(cake_model* m, long long* n, int reset);
  * pairs, bits 4/5 drop the L2 evict_last hint of A / B, bit6 no K-split of
  * the short last gate/up round, bit7 QKV on N-256 tiles instead of N-192. Default 0. */
 CAKE_API int cake_gemm_set_schedule(int schedule);
+/* A/B switches for measurements only (process-wide; the defaults are the product):
+ * PDL 1 = programmatic dependent launch on; FUSED_NORM 1 = RMSNorm folded into the
+ * projections; ATTN_MAX_WAVES = CTA waves the split-KV dispatch may use (1);
+ * GEMM_NOSPLIT 1 = no split-K for the few-tile pair GEMMs (0). */
+enum { CAKE_EXP_PDL = 0, CAKE_EXP_FUSED_NORM = 1, CAKE_EXP_ATTN_MAX_WAVES = 2, CAKE_EXP_GEMM_NOSPLIT = 3,
+       CAKE_EXP_COUNT = 4 };
+CAKE_API int cake_set_experiment(int knob, int value);
 /* C = A · B^T for bf16 row-major A [M, K], B [N, K]; epi 0: bf16 C, 1: fp32 C,
  * 2: fp32 C += . block_n 128 or 256. For tests and microbenchmarks. */
 CAKE_API int cake_gemm(const void* dA, const void* dB, void* dC, int M, int N, int K, int epi, int block_n,

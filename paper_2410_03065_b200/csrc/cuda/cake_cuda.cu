@@ -74,14 +74,11 @@ cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 // launched here calls pdl_wait() before touching its predecessor's outputs):
 // the next kernel's CTAs become resident and run their prologue (barrier
 // init, TMEM alloc, descriptor prefetch) while the previous kernel drains.
-// CAKE_PDL=0 turns it off (A/B measurements).
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("CAKE_PDL");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
+// A/B switches for measurements (cake_set_experiment); the defaults are the product.
+int g_exp[CAKE_EXP_COUNT] = {1 /*PDL*/, 1 /*FUSED_NORM*/, 1 /*ATTN_MAX_WAVES*/, 0 /*GEMM_NOSPLIT*/};
+
+// cake_set_experiment(CAKE_EXP_PDL, 0) turns programmatic dependent launch off.
+bool pdl_enabled() { return g_exp[CAKE_EXP_PDL] != 0; }
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_chain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster,
@@ -323,7 +320,6 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
     }
     max_pairs = std::min(n, num_sms() / 2);
     pairs_for_sms = num_sms();
-    if (std::getenv("CAKE_DEBUG_GEMM")) std::fprintf(stderr, "gemm2: occupancy reports %d co-resident pairs\n", n);
   }
   a.num_m_blocks = (a.M + kGemmBlockM - 1) / kGemmBlockM;
   a.num_n_blocks = a.N / BLOCK_N;
@@ -339,8 +335,7 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
   } else {
     // split parts run concurrently (the owner waits for its partner): keep
     // tiles * split within the SM pairs so every part is resident together
-    static const bool no_split = std::getenv("CAKE_GEMM_NOSPLIT") != nullptr;  // experiments: one pair per tile
-    const int pair_budget = no_split ? 0 : num_sms() / 2;
+    const int pair_budget = g_exp[CAKE_EXP_GEMM_NOSPLIT] ? 0 : num_sms() / 2;  // experiment: one pair per tile
     int split = 1;
     while (tiles * (split + 1) <= pair_budget && a.num_k_blocks % (split + 1) == 0 &&
            a.num_k_blocks / (split + 1) >= 8)
@@ -770,7 +765,7 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
     // two waves of short splits slower than one of longer splits (first-token
     // step attention 1.40 -> 1.16 ms at 32K: 18 splits instead of 37)
     const int max_s = std::max(1, std::min({n_pages / 8, m->max_splits, cap}));
-    static const int max_waves = std::getenv("CAKE_ATTN_MAX_WAVES") ? std::atoi(std::getenv("CAKE_ATTN_MAX_WAVES")) : 1;
+    const int max_waves = std::max(1, g_exp[CAKE_EXP_ATTN_MAX_WAVES]);
     double best = 0.0;
     for (int sp = 1; sp <= max_s; ++sp) {
       const int ctas = base_ctas * sp;
@@ -1001,13 +996,9 @@ int last_token_pass(cake_model* m, const int32_t* d_token, long long T, const in
 // epilogues of O / down write bf16(h) and per-tile sums of squares, the next
 // QKV / gate-up epilogue applies the row scale. Single-GPU only (the TP path
 // adds the all-reduced partials in a separate kernel and keeps rmsnorm).
-// CAKE_FUSED_NORM=0 restores the standalone kernel (A/B measurements).
+// cake_set_experiment(CAKE_EXP_FUSED_NORM, 0) restores the standalone kernel (A/B measurements).
 bool fused_norm(const cake_model* m) {
-  static const bool on = [] {
-    const char* e = std::getenv("CAKE_FUSED_NORM");
-    return !(e && e[0] == '0');
-  }();
-  return on && m->cfg.tp_size == 1 && !m->emulated_tp && m->H % 128 == 0;
+  return g_exp[CAKE_EXP_FUSED_NORM] != 0 && m->cfg.tp_size == 1 && !m->emulated_tp && m->H % 128 == 0;
 }
 
 void set_norm_consumer(cake_model* m, GemmArgs& g) {
@@ -1805,6 +1796,12 @@ int cake_gemm_set_schedule(int schedule) {
   g_gemm_schedule = schedule & 1;
   g_gemm_2sm = (schedule & 2) ? 0 : 1;
   g_gemm_cluster = (schedule & 4) ? 1 : 0;
+  return CAKE_OK;
+}
+
+int cake_set_experiment(int knob, int value) {
+  if (knob < 0 || knob >= CAKE_EXP_COUNT) return fail(CAKE_EINVAL, "experiment knob %d out of range", knob);
+  g_exp[knob] = value;
   return CAKE_OK;
 }
 

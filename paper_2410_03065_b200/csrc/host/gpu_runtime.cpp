@@ -918,12 +918,9 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   const long long T = static_cast<long long>(tail.token_start + tail.token_count);
   if (tp) tp->publish_final(tail_hidden ? 0 : 1, static_cast<int>(tail.token_count) - 1);
   check(cake_event_record(g.ev_final_start->h, g.s_compute), "record");
-  const Micros enq0 = timer.now_us();
   check(cake_final_logits(g.model, T, g.tokens.p + (T - 1), tail_hidden ? 0 : 1, static_cast<int>(tail.token_count) - 1,
                           g.final_bt, g.logits.p, g.s_compute),
         "final logits");
-  if (std::getenv("CAKE_DEBUG_FINAL"))
-    std::fprintf(stderr, "final step: host enqueue %lld us\n", static_cast<long long>(timer.now_us() - enq0));
   check(cake_d2h_async(g.h_logits.p, g.logits.p, g.cfg.vocab * sizeof(float), g.s_compute), "logits D2H");
   check(cake_event_record(g.ev_logits->h, g.s_compute), "record");
   check(cake_event_sync(g.ev_logits->h), "logits");

@@ -26,6 +26,17 @@ def test_reference_suites_pass_on_reference():
     assert "0 failed" in p.stdout
 
 
+@pytest.mark.parametrize("name", ["acceptance_ref", "acceptance_b200"])
+def test_reference_acceptance_main(name):
+    """proj/tests/acceptance.cpp:498-527 — the reference's 10 acceptance criteria
+    (near-optimality, exactly-once under jitter, dominance, merge trend, collapse,
+    live throttle fidelity, scheduler overhead, codec equivalence, store
+    integrity, reproducibility), against the reference and against libcake.so."""
+    p = _run(name)
+    assert p.returncode == 0, (p.stdout[-3000:], p.stderr[-3000:])
+    assert "acceptance: all criteria passed" in p.stdout, p.stdout[-3000:]
+
+
 def test_reference_suites_pass_on_b200_library():
     p = _run("unit_b200")
     assert p.returncode == 0, p.stderr[-4000:]
