@@ -259,7 +259,7 @@ def b200_arm(args):
     base_c = min((one("compute_only")[0] for _ in range(2)), key=lambda r: r.first_token_ms)
     base_io = min((one("io_only")[0] for _ in range(2)), key=lambda r: r.first_token_ms)
     # warm-up 1 is fully event-bracketed: the per-kernel breakdown ("kernels") and
-    # the choice of the dominant kernel class; the timed steps bracket only that class
+    # the choice of the dominant kernel class
     rt.set_profiling("all")
     one()
     breakdown = rt.kernel_stats(reset=True)
@@ -268,10 +268,6 @@ def b200_arm(args):
     for _ in range(args.warmup - 1):
         one()
     rt.kernel_stats(reset=True)
-    if args.profile:
-        # every 4th launch of the dominant class is event-bracketed in the timed steps: a
-        # live sample of its duration that leaves 3 of 4 programmatic-launch chains intact
-        rt.set_profiling([dom_name], stride=4)
 
     def barrier():
         if dist:
@@ -280,6 +276,7 @@ def b200_arm(args):
             torch.cuda.synchronize()
             dist.barrier()
 
+    # timed steps: no event brackets (every programmatic-launch chain intact)
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
@@ -290,8 +287,16 @@ def b200_arm(args):
         walls.append(w)
     barrier()
     clk = clocks.stop()
-    stats = rt.kernel_stats(reset=True)
-    rt.set_profiling(None, stride=1)
+    stats = None
+    if args.profile:
+        # roofline steps, right after the timed region on the same warm state: every
+        # launch of the dominant class is bracketed by CUDA events on its own stream
+        rt.kernel_stats(reset=True)
+        rt.set_profiling([dom_name], stride=1)
+        for _ in range(max(1, min(args.steps, 3))):
+            one()
+        stats = rt.kernel_stats(reset=True)
+        rt.set_profiling(None, stride=1)
 
     dev = statistics.mean(r.device_ttft_ms for r in res)
     e2e = statistics.mean(r.first_token_ms for r in res)
@@ -310,8 +315,8 @@ def b200_arm(args):
     # dominant kernel class, timed live in the timed region (CUDA events bracketing
     # each of its launches on its own stream); its share from the bracketed warm-up
     total = sum(v["ms"] for v in breakdown.values()) or 1.0
-    d = stats[dom_name] if stats[dom_name]["launches"] else breakdown[dom_name]
-    tensor_bound = d["flops"] > 0 and d["flops"] / max(d["bytes"], 1) > 300
+    d = stats[dom_name] if stats and stats[dom_name]["launches"] else breakdown[dom_name]
+    tensor_bound = is_tensor_bound(d)
     if tensor_bound:
         achieved = d["flops"] / (d["ms"] / 1e3) / 1e12
         rl = {"bound": "tensor", "achieved": achieved, "peak": peak_s, "unit": "TFLOP/s", "frac": achieved / peak_s}
@@ -323,10 +328,7 @@ def b200_arm(args):
                "per_launch_ms": d["ms"] / max(1, d["launches"]),
                "peak_kind": f"{peak_kind} bf16 sustained" if tensor_bound else f"{peak_kind} hbm",
                "traffic": traffic_from_profiles(dom_name)})
-    kernels = {k: {"ms_per_step": v["ms"], "launches_per_step": v["launches"],
-                   "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 and v["flops"] > 0 else None,
-                   "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else None}
-               for k, v in breakdown.items() if v["launches"]}
+    kernels = {k: class_roofline(v, peak_s, hbm) for k, v in breakdown.items() if v["launches"]}
     line = {
         "metric": METRIC, "value": dev, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": wall, "higher_is_better": False, "scaling": "strong",
@@ -355,6 +357,26 @@ def b200_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def is_tensor_bound(v):
+    """Arithmetic intensity above the B200 ridge (~200 FLOP/B): tensor-pipe bound."""
+    return v["flops"] > 0 and v["flops"] / max(v["bytes"], 1) > 300
+
+
+def class_roofline(v, peak_tflops, hbm_gbs):
+    """Per-class line of the bracketed warm-up step: time, launches, achieved rate
+    against the roof that bounds the class (bf16 sustained or HBM)."""
+    ms = v["ms"]
+    out = {"ms_per_step": ms, "launches_per_step": v["launches"],
+           "tflops": (v["flops"] / (ms / 1e3) / 1e12) if ms > 0 and v["flops"] > 0 else None,
+           "gbs": (v["bytes"] / (ms / 1e3) / 1e9) if ms > 0 else None}
+    if ms > 0 and (v["flops"] > 0 or v["bytes"] > 0):
+        if is_tensor_bound(v):
+            out.update(bound="tensor", frac=out["tflops"] / peak_tflops)
+        else:
+            out.update(bound="hbm", frac=out["gbs"] / hbm_gbs)
+    return out
+
+
 def traffic_from_profiles(kernel):
     """dram bytes per launch for `kernel` from the committed ncu summary, if any."""
     try:
@@ -377,6 +399,16 @@ def main():
     ap.add_argument("--no-profile", dest="profile", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: launch our own ranks when not started by torchrun
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.run(cmd).returncode)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

@@ -203,6 +203,8 @@ enum {
   CAKE_K_ALLREDUCE,
   CAKE_K_LMHEAD,
   CAKE_K_SCATTER,
+  CAKE_K_DEC_PROJ, /* first-token step: the weight-streaming q / o / gate-up / down GEMVs */
+  CAKE_K_DEC_ATTN, /* first-token step: 1-query attention over the assembled cache */
   CAKE_K_COUNT
 };
 typedef struct cake_kernel_stat {

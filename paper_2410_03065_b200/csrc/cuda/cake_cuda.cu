@@ -408,7 +408,9 @@ int launch_gemm2c(const CUtensorMap& ta_piece, const CUtensorMap& tb_half, const
   const int clusters = std::max(1, std::min(tiles, max_clusters));
   // output maps (h fp32, bf16(h)): the staged residual epilogue, one tile per CTA
   a.prefetch = g_gemm_prefetch;
-  a.staged = (EPI == kEpiResid && BLOCK_N == 128 && om != nullptr && tiles <= clusters) ? 1 : 0;
+  // (the staging boxes reuse the operand ring: 4 x 16 KB of h + 2 x 16 KB of bf16(h))
+  constexpr bool ring_fits = Cfg::kStages * Cfg::kStageBytes >= 6 * 128 * 128;
+  a.staged = (ring_fits && EPI == kEpiResid && BLOCK_N == 128 && om != nullptr && tiles <= clusters) ? 1 : 0;
   const CUtensorMap& th = a.staged ? om[0] : ta_piece;
   const CUtensorMap& tx = a.staged ? om[1] : ta_piece;
   CK(launch_chain(kern, dim3(2 * NP * clusters), dim3(kGemmThreads), Cfg::kSmemBytes, s, 2 * NP, ta_piece, tb_half,
@@ -693,7 +695,7 @@ int attention_fa4(cake_model* m, long long chunk_start, int chunk_len, int layer
   const double vis = static_cast<double>(chunk_len) * chunk_start + 0.5 * chunk_len * (chunk_len + 1.0);
   const double flops = 4.0 * m->hd * m->nq * vis;
   const double bytes = static_cast<double>(kv_end) * m->nkv * m->hd * 2 * 2 + 2.0 * chunk_len * m->nq * m->hd * 2;
-  ProfScope ps(m, CAKE_K_ATTN, s, flops, bytes);
+  ProfScope ps(m, chunk_len == 1 ? CAKE_K_DEC_ATTN : CAKE_K_ATTN, s, flops, bytes);
   F4Args fa{};
   fa.fa.q = m->q;
   fa.fa.block_table = bt;
@@ -785,7 +787,7 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
   const double vis = static_cast<double>(chunk_len) * chunk_start + 0.5 * chunk_len * (chunk_len + 1.0);
   const double flops = 4.0 * m->hd * m->nq * vis;
   const double bytes = static_cast<double>(kv_end) * m->nkv * m->hd * 2 * 2 + 2.0 * chunk_len * m->nq * m->hd * 2;
-  ProfScope ps(m, CAKE_K_ATTN, s, flops, bytes);
+  ProfScope ps(m, chunk_len == 1 ? CAKE_K_DEC_ATTN : CAKE_K_ATTN, s, flops, bytes);
   dim3 grid(qtiles, m->nkv, splits);
   if (tc) {
     FaArgs fa;
@@ -969,10 +971,10 @@ int last_token_pass(cake_model* m, const int32_t* d_token, long long T, const in
       a.rope = m->rope;
       a.pos0 = T - 1;
       a.head_dim = m->hd;
-      CKS(launch_skinny<kSkQRope>(m, CAKE_K_GEMM_QKV, a, m->nq * m->hd, s));
+      CKS(launch_skinny<kSkQRope>(m, CAKE_K_DEC_PROJ, a, m->nq * m->hd, s));
     }
     CKS(attention(m, T - 1, 1, l, bt, nullptr, s));
-    CKS(skinny_row_parallel(m, CAKE_K_GEMM_O, lw.wo, m->attn, m->nq * m->hd, s));
+    CKS(skinny_row_parallel(m, CAKE_K_DEC_PROJ, lw.wo, m->attn, m->nq * m->hd, s));
     {
       SkinnyArgs a{};
       a.W = lw.wgu;
@@ -985,9 +987,9 @@ int last_token_pass(cake_model* m, const int32_t* d_token, long long T, const in
       a.units = m->F;
       a.act = m->act;
       a.ld_act = m->F;
-      CKS(launch_skinny<kSkSwiglu>(m, CAKE_K_GEMM_GU, a, 2.0 * m->F, s));
+      CKS(launch_skinny<kSkSwiglu>(m, CAKE_K_DEC_PROJ, a, 2.0 * m->F, s));
     }
-    CKS(skinny_row_parallel(m, CAKE_K_GEMM_D, lw.wd, m->act, m->F, s));
+    CKS(skinny_row_parallel(m, CAKE_K_DEC_PROJ, lw.wd, m->act, m->F, s));
   }
   return CAKE_OK;
 }

@@ -23,6 +23,9 @@
 
 namespace cake_dev {
 
+#ifndef CAKE_GEMM_RING_KB
+#define CAKE_GEMM_RING_KB 200
+#endif
 template <int BLOCK_N>
 struct Gemm2Cfg {
   static_assert(BLOCK_N % 32 == 0 && BLOCK_N >= 64 && BLOCK_N <= 256, "cta_group::2 tile N");
@@ -31,7 +34,7 @@ struct Gemm2Cfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   // 6 (N 256) .. 8 (N 128). A/B of the ring budget 176 / 200 / 224 KB: within 1-2% per
   // shape, no trend (the depth is not what bounds the mainloop)
-  static constexpr int kStages = (200 * 1024) / kStageBytes;
+  static constexpr int kStages = (CAKE_GEMM_RING_KB * 1024) / kStageBytes;
   static constexpr int kTmemCols = (2 * BLOCK_N <= 256) ? 256 : 512;       // 2 accumulators
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 };

@@ -62,7 +62,7 @@ class CakeKernelStat(C.Structure):
 
 
 KERNEL_NAMES = ["embed", "rmsnorm", "gemm_qkv", "attention", "gemm_o", "gemm_gu", "gemm_down", "allreduce",
-                "lm_head", "kv_scatter"]
+                "lm_head", "kv_scatter", "dec_proj", "dec_attn"]
 
 P = C.POINTER
 _SIGS = {

@@ -34,7 +34,13 @@ def cos(a, b):
     return float(np.dot(a, b) / (np.linalg.norm(a) * np.linalg.norm(b)))
 
 
+MIN_MARGIN = 0.02  # the oracle's top-1 lead over the runner-up, in logits RMS (see test_gpu_parity.py)
+
+
 def logits_ok(got, want, what=""):
+    w = np.sort(np.asarray(want, np.float64))[::-1]
+    margin = float((w[0] - w[1]) / np.sqrt(np.mean(w ** 2)))
+    assert margin >= MIN_MARGIN, ("ill-posed top-1 check: pick another prompt seed", what, margin)
     assert np.isfinite(got).all(), what
     e = rms_rel(got, want)
     assert e <= TOL, (what, e)

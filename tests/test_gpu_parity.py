@@ -22,13 +22,17 @@ TOL = 2.0 ** -7
 NAN = 0xFF  # poison byte: 0xFFFF is a bf16 NaN
 
 CONFIGS = {
-    # name: (dims, T, chunk)
-    "tiny": ((2, 256, 4, 4, 64, 1024, 32000), 2048, 256),
-    "gqa_hd64": ((2, 512, 8, 2, 64, 1024, 32000), 1024, 256),
-    "gqa_hd128": ((2, 1024, 8, 2, 128, 2048, 32768), 1024, 512),
+    # name: (dims, T, chunk, prompt seed)
+    "tiny": ((2, 256, 4, 4, 64, 1024, 32000), 2048, 256, 44),
+    "gqa_hd64": ((2, 512, 8, 2, 64, 1024, 32000), 1024, 256, 42),
+    "gqa_hd128": ((2, 1024, 8, 2, 128, 2048, 32768), 1024, 512, 45),
     # GQA 8:1 (the Llama-3-70B grouping: 16 tokens x 8 heads per 128-row tile)
-    "gqa8_hd128": ((2, 1024, 16, 2, 128, 2048, 32768), 1024, 256),
+    "gqa8_hd128": ((2, 1024, 16, 2, 128, 2048, 32768), 1024, 256, 45),
 }
+# Prompt seeds are chosen so the oracle's top-1 is DECIDABLE at bf16: its lead over
+# the runner-up is >= MIN_MARGIN of the logits' RMS (seed 42 on gqa_hd128 has a
+# 0.2% lead, inside the bf16 noise, and flips with any change of summation order).
+MIN_MARGIN = 0.02
 
 
 def rms_rel(a, b):
@@ -41,7 +45,13 @@ def cos(a, b):
     return float(np.dot(a, b) / (np.linalg.norm(a) * np.linalg.norm(b)))
 
 
+def top1_margin(want):
+    w = np.sort(np.asarray(want, np.float64))[::-1]
+    return float((w[0] - w[1]) / np.sqrt(np.mean(w ** 2)))
+
+
 def logits_ok(got, want):
+    assert top1_margin(want) >= MIN_MARGIN, ("ill-posed top-1 check: pick another prompt seed", top1_margin(want))
     assert np.isfinite(got).all()
     assert rms_rel(got, want) <= TOL, rms_rel(got, want)
     assert cos(got, want) >= 0.999
@@ -64,8 +74,7 @@ def setup(request):
     from paper_2410_03065_b200.cake import Cake
     from paper_2410_03065_b200.runtime import GpuRuntime
 
-    dims, T, C = CONFIGS[request.param]
-    seed = 42
+    dims, T, C, seed = CONFIGS[request.param]
     rt = GpuRuntime(dims, max_tokens=T, max_chunk=C)
     rt.poison(NAN)
     tier = rt.build_cache_tier(T, C, seed)
@@ -82,7 +91,7 @@ def setup(request):
     base_logits = rt.logits()
     prun(rt, tier, T, C, seed, mbps=64000, mode="io_only")
     io_logits = rt.logits()
-    return {"rt": rt, "tier": tier, "ref": ref, "toks": toks, "T": T, "C": C, "dims": dims, "keys": keys,
+    return {"rt": rt, "tier": tier, "ref": ref, "toks": toks, "T": T, "C": C, "dims": dims, "keys": keys, "seed": seed,
             "ref_logits": ref.final_logits(C - 1), "base_kv": base_kv, "base_logits": base_logits,
             "io_logits": io_logits}
 
@@ -103,7 +112,7 @@ def test_tier_holds_the_computed_cache(setup):
 
 def test_computed_kv_matches_oracle(setup):
     rt, T, C = setup["rt"], setup["T"], setup["C"]
-    prun(rt, setup["tier"], T, C, 42, mbps=1000, mode="compute_only")
+    prun(rt, setup["tier"], T, C, setup["seed"], mbps=1000, mode="compute_only")
     kv = setup["ref"].kv()
     for s in range(0, T, C):
         got = _chunk_kv(rt, s, C)
@@ -117,7 +126,7 @@ def test_computed_kv_matches_oracle(setup):
 @pytest.mark.parametrize("mode", ["compute_only", "io_only"])
 def test_first_token_logits_match_oracle(setup, mode):
     rt = setup["rt"]
-    r = prun(rt, setup["tier"], setup["T"], setup["C"], 42, mbps=4000, mode=mode)
+    r = prun(rt, setup["tier"], setup["T"], setup["C"], setup["seed"], mbps=4000, mode=mode)
     assert r.recomputed_last == (mode == "io_only")
     logits_ok(rt.logits(), setup["ref_logits"])
 
@@ -125,7 +134,7 @@ def test_first_token_logits_match_oracle(setup, mode):
 def test_loaded_kv_bit_exact(setup):
     """I/O-only from a poisoned pool: every page was landed by the loader, byte for byte."""
     rt, T, C = setup["rt"], setup["T"], setup["C"]
-    r = prun(rt, setup["tier"], T, C, 42, mbps=40000, mode="io_only")
+    r = prun(rt, setup["tier"], T, C, setup["seed"], mbps=40000, mode="io_only")
     assert r.merge_point == 0
     assert all(c.side == "io" for c in r.chunks)
     for i, s in enumerate(range(0, T, C)):
@@ -136,7 +145,7 @@ def test_loaded_kv_bit_exact(setup):
 @pytest.mark.parametrize("mbps", [200, 2000, 20000, 200000])
 def test_assembled_cache_independent_of_merge_point(setup, mbps):
     rt, T, C = setup["rt"], setup["T"], setup["C"]
-    r = prun(rt, setup["tier"], T, C, 42, mbps=mbps, mode="cake")
+    r = prun(rt, setup["tier"], T, C, setup["seed"], mbps=mbps, mode="cake")
     assert sorted(c.index for c in r.chunks) == list(range(T // C))
     for i, s in enumerate(range(0, T, C)):
         assert rt.read_chunk(s, C) == setup["base_kv"][i], (mbps, i, r.merge_point)
@@ -166,7 +175,7 @@ def test_forced_boundary_race(setup, case):
     spec = RACES[case]
     n = T // C
     quantum = (1 << 20) if spec["racer"] == "compute" else rt.kv_bytes_per_token * C
-    r = prun(rt, setup["tier"], T, C, 42, mbps=spec["mbps"], mode="cake", quantum=quantum,
+    r = prun(rt, setup["tier"], T, C, setup["seed"], mbps=spec["mbps"], mode="cake", quantum=quantum,
              race_force=spec["race_force"], race_hold=spec["race_hold"])
     assert r.raced_chunk >= 0, case
     assert r.race_winner == spec["winner"], (case, r.raced_chunk, r.race_winner)
@@ -191,7 +200,7 @@ def test_tcgen05_attention_matches_mma_sync_kernel(setup):
     rt, T, C = setup["rt"], setup["T"], setup["C"]
     rt.set_attention_impl("mma_sync")
     try:
-        prun(rt, setup["tier"], T, C, 42, mbps=1000, mode="compute_only")
+        prun(rt, setup["tier"], T, C, setup["seed"], mbps=1000, mode="compute_only")
         mma = [_chunk_kv(rt, s, C) for s in range(0, T, C)]
         lg_mma = rt.logits()
     finally:
@@ -216,8 +225,8 @@ def test_partially_cached_prompt(setup, mode):
     and the first-token logits are bit-identical to a full compute-only run."""
     rt, T, C = setup["rt"], setup["T"], setup["C"]
     cached = T // 2
-    part = rt.build_cache_tier(cached, C, 42)
-    r = prun(rt, part, T, C, 42, mbps=1000, mode=mode, cached_prefix=True)
+    part = rt.build_cache_tier(cached, C, setup["seed"])
+    r = prun(rt, part, T, C, setup["seed"], mbps=1000, mode=mode, cached_prefix=True)
     assert r.n_chunks == T // C
     assert sorted(c.index for c in r.chunks) == list(range(T // C))
     assert all(c.side == "compute" for c in r.chunks if c.index >= cached // C)
@@ -226,7 +235,7 @@ def test_partially_cached_prompt(setup, mode):
     assert [rt.read_chunk(s, C) for s in range(0, T, C)] == setup["base_kv"]
     assert np.array_equal(rt.logits(), setup["base_logits"])
     with pytest.raises(Exception):
-        rt.run(part, T, C, 42, mbps=1000, mode=mode)  # without the option a missing chunk is an error
+        rt.run(part, T, C, setup["seed"], mbps=1000, mode=mode)  # without the option a missing chunk is an error
 
 
 @pytest.mark.parametrize("direct", [False, True])
@@ -238,10 +247,10 @@ def test_file_tier(setup, tmp_path, direct):
 
     rt, T, C = setup["rt"], setup["T"], setup["C"]
     fs = ChunkStore(rt.n, str(tmp_path / f"tier{int(direct)}"), create=1)
-    rt.build_cache_tier(T, C, 42, store=fs)
+    rt.build_cache_tier(T, C, setup["seed"], store=fs)
     fs.set_direct_io(direct)
     for mode in ("io_only", "cake"):
-        r = prun(rt, fs, T, C, 42, mbps=8000, mode=mode)
+        r = prun(rt, fs, T, C, setup["seed"], mbps=8000, mode=mode)
         assert sorted(c.index for c in r.chunks) == list(range(T // C))
         assert [rt.read_chunk(s, C) for s in range(0, T, C)] == setup["base_kv"]
         assert np.array_equal(rt.logits(), setup["io_logits"] if r.recomputed_last else setup["base_logits"])
@@ -260,14 +269,14 @@ def test_sm_share_compute_stream(setup):
     small = GpuRuntime(setup["dims"], max_tokens=T, max_chunk=C, compute_sms=16)
     try:
         small.poison(NAN)
-        tier = small.build_cache_tier(T, C, 42)
-        prun(small, tier, T, C, 42, mbps=1000, mode="compute_only")
+        tier = small.build_cache_tier(T, C, setup["seed"])
+        prun(small, tier, T, C, setup["seed"], mbps=1000, mode="compute_only")
         base = [small.read_chunk(s, C) for s in range(0, T, C)]
         base_lg = small.logits()
         for i, s in enumerate(range(0, T, C)):
             assert rms_rel(_chunk_kv(small, s, C), _base(setup, i)) <= TOL
         assert rms_rel(base_lg, setup["base_logits"]) <= TOL
-        r = prun(small, tier, T, C, 42, mbps=1000, mode="cake")
+        r = prun(small, tier, T, C, setup["seed"], mbps=1000, mode="cake")
         assert sorted(c.index for c in r.chunks) == list(range(T // C))
         assert [small.read_chunk(s, C) for s in range(0, T, C)] == base
         tier.close()
