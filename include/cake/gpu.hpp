@@ -72,6 +72,9 @@ struct GpuOptions {
   // GPU share of the compute side: > 0 confines the
   // compute stream to this many SMs (green context); 0 = the whole GPU.
   int compute_sms = 0;
+  // Share this context's weights (same dimensions, seed and TP shard; it must
+  // outlive the new context): one context per concurrent request on a device.
+  const GpuContext* weights_from = nullptr;
 };
 
 struct GpuRunInfo {

@@ -79,6 +79,7 @@ typedef struct cake_run_opts {
   int record_slices;  /* log every released slice (TransferOptions::record_slices) */
   int race_force;     /* test instrumentation (RunOptions::race_force): 0 policy, 1 compute contests, 2 io contests */
   int race_hold;      /* test instrumentation (RunOptions::race_hold): -1 off, 0 compute waits, 1 io waits */
+  void* link;         /* B200 extension: a cake_link* the loader paces through (shared with other runs), or NULL */
 } cake_run_opts;
 
 typedef struct cake_summary {
@@ -150,6 +151,8 @@ typedef struct cake_gpu_config {
   int64_t race_margin_us;
   const char* tp_shm; /* POSIX shm name of the TP group's coordinator (tp_size > 1), NULL otherwise */
   int compute_sms;    /* > 0: confine the compute stream to this many SMs (GPU-share emulation) */
+  const struct cake_gpu* weights_from; /* non-NULL: share this context's weights (same dims, seed, TP shard;
+                                          it must outlive the new one) — concurrent requests on one device */
 } cake_gpu_config;
 
 typedef struct cake_gpu_result {
@@ -170,6 +173,17 @@ typedef struct cake_gpu_result {
 } cake_gpu_result;
 
 CAKE_API int cake_gpu_create(const cake_gpu_config* cfg, cake_gpu** out);
+/* One emulated link shared by several contexts' loaders (concurrent requests
+ * on one device): every slice of every attached context reserves the next slot
+ * of one budget clock over `trace` (t = 0 at creation / reset). No reference
+ * counterpart: the reference serves one request per process. */
+typedef struct cake_link cake_link;
+CAKE_API int cake_link_create(cake_trace trace, cake_link** out);
+CAKE_API int cake_link_destroy(cake_link* l);
+CAKE_API int cake_link_reset(cake_link* l);  /* only while no attached run is in flight */
+CAKE_API int cake_link_reserved_bits(const cake_link* l, uint64_t* bits, int64_t* now_us);
+/* Attach (l != NULL) or detach: later runs of g pace through l instead of their own trace. */
+CAKE_API int cake_gpu_set_link(cake_gpu* g, cake_link* l);
 CAKE_API int cake_gpu_destroy(cake_gpu* g);
 CAKE_API int cake_gpu_kv_bytes_per_token(const cake_gpu* g, uint64_t* out);
 /* Fill `store` (create it memory-resident+pinned) from a compute-only GPU pass. */

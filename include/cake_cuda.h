@@ -121,6 +121,10 @@ typedef struct cake_model_info {
 typedef struct cake_model cake_model;
 
 CAKE_API int cake_model_create(const cake_model_config* cfg, cake_model** out);
+/* A model that shares `parent`'s weights (same dimensions, seed and TP shard;
+ * `parent` must outlive it) and owns its own paged pool and scratch: one
+ * context per concurrent request on a device, weights resident once. */
+CAKE_API int cake_model_create_shared(const cake_model_config* cfg, const cake_model* parent, cake_model** out);
 CAKE_API int cake_model_destroy(cake_model* m);
 CAKE_API int cake_model_get_info(const cake_model* m, cake_model_info* out);
 /* Attention kernel variant: 0 = product dispatch (the one-tile tcgen05/TMEM

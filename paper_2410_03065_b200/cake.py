@@ -91,7 +91,9 @@ def _opts(lib: N.Native, **kw) -> N.CakeRunOpts:
     for k, v in kw.items():
         if not hasattr(o, k):
             raise TypeError(f"unknown run option {k}")
-        setattr(o, k, int(v) if not isinstance(v, float) else v)
+        if k == "link":
+            v = v.h if v is not None else None  # a runtime.Link
+        setattr(o, k, v if v is None or isinstance(v, float) else int(v))
     return o
 
 

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -179,16 +180,19 @@ int num_sms() {
   return g_sm_limit > 0 ? std::min(g_sm_limit, g_num_sms) : g_num_sms;
 }
 
-// Stream-K scratch shared by every GEMM launch of the process (launches are
-// stream-ordered on one compute stream per device; the epoch keeps flags of
-// consecutive launches apart without a reset).
+// Stream-K / split-K scratch, one set per launching stream: launches on one
+// stream reuse it in stream order (the epoch keeps flags of consecutive
+// launches apart without a reset); concurrent contexts (one compute stream
+// each) never share it.
 struct StreamKScratch {
   float* ws = nullptr;
   int* flags = nullptr;
   int epoch = 0;
-  std::mutex mu;
+  float* tail_ws = nullptr;  // gate/up tail-split partials (whole_tiles == 2)
+  size_t tail_floats = 0;
 };
-StreamKScratch g_sk;
+std::mutex g_sk_mu;
+std::unordered_map<cudaStream_t, StreamKScratch> g_sk;
 int g_gemm_schedule = 0;  // 0 whole tiles (+ exact split-K when tiles < SM pairs), 1 stream-K
 int g_gemm_2sm = 1;       // 1: M > 128 projections use the 2-SM (cta_group::2) kernel
 int g_gemm_2sm_n128 = 1;  // O / down (N tiles of 128) on CTA pairs: down 59.9 -> 54.0 us at M = 512
@@ -199,30 +203,33 @@ int g_gemm_pairs = 2;       // > 1: N-128/192 projections in clusters of this ma
 int g_gemm_qkv192 = 1;      // QKV on CTA-pair tiles of N 192 (rope-unit weight rows) when the rows tile
 
 // Tail-split partials of whole_tiles == 2 launches (stream-ordered reuse).
-float* g_tail_ws = nullptr;
-size_t g_tail_floats = 0;
-int tail_scratch(float** ws, size_t floats) {
-  std::lock_guard<std::mutex> lk(g_sk.mu);
-  if (floats > g_tail_floats) {
-    if (g_tail_ws) CK(cudaFree(g_tail_ws));
-    CK(cudaMalloc(&g_tail_ws, floats * sizeof(float)));
-    g_tail_floats = floats;
+int tail_scratch(float** ws, size_t floats, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_sk_mu);
+  StreamKScratch& k = g_sk[s];
+  if (floats > k.tail_floats) {
+    if (k.tail_ws) CK(cudaFree(k.tail_ws));
+    CK(cudaMalloc(&k.tail_ws, floats * sizeof(float)));
+    k.tail_floats = floats;
   }
-  *ws = g_tail_ws;
+  *ws = k.tail_ws;
   return CAKE_OK;
 }
 
-int streamk_scratch(float** ws, int** flags, int* epoch) {
-  std::lock_guard<std::mutex> lk(g_sk.mu);
-  if (!g_sk.ws) {
-    const size_t slots = static_cast<size_t>(num_sms());
-    CK(cudaMalloc(&g_sk.ws, slots * kGemmBlockM * 256 * sizeof(float)));
-    CK(cudaMalloc(&g_sk.flags, slots * sizeof(int)));
-    CK(cudaMemset(g_sk.flags, 0, slots * sizeof(int)));
+int streamk_scratch(float** ws, int** flags, int* epoch, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(g_sk_mu);
+  StreamKScratch& k = g_sk[s];
+  if (!k.ws) {
+    // slots for the whole device, not the current SM budget: a stream handle
+    // can be reused by a later context with a larger budget
+    num_sms();
+    const size_t slots = static_cast<size_t>(g_num_sms);
+    CK(cudaMalloc(&k.ws, slots * kGemmBlockM * 256 * sizeof(float)));
+    CK(cudaMalloc(&k.flags, slots * sizeof(int)));
+    CK(cudaMemset(k.flags, 0, slots * sizeof(int)));
   }
-  *ws = g_sk.ws;
-  *flags = g_sk.flags;
-  *epoch = ++g_sk.epoch;
+  *ws = k.ws;
+  *flags = k.flags;
+  *epoch = ++k.epoch;
   return CAKE_OK;
 }
 
@@ -281,7 +288,7 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmArgs a, cudaSt
   // stream-K: every cluster gets >= 8 k-blocks (>= 1 unit, so none is empty); all clusters co-resident
   const long long work = a.whole_tiles ? static_cast<long long>(m_groups) * a.num_n_blocks : units / 8;
   const int clusters = static_cast<int>(std::max<long long>(1, std::min<long long>(max_clusters[ci], work)));
-  CKS(streamk_scratch(&a.sk_ws, &a.sk_flags, &a.epoch));
+  CKS(streamk_scratch(&a.sk_ws, &a.sk_flags, &a.epoch, s));
   CK(launch_chain(kern, dim3(clusters * a.cs), dim3(kGemmThreads), Cfg::kSmemBytes, s, a.cs, ta, tb, a));
   return CAKE_OK;
 }
@@ -348,11 +355,11 @@ int launch_gemm2(const CUtensorMap& ta, const CUtensorMap& tb_half, GemmArgs a, 
       const int r = tiles % pairs;
       if (split == 1 && g_gemm_tail_split && tiles > pairs && r > 0 && 2 * r <= pairs && a.num_k_blocks >= 16) {
         a.whole_tiles = 2;
-        CKS(tail_scratch(&a.tail_ws, static_cast<size_t>(r) * tail_parts(r, pairs) * 256 * 256));
+        CKS(tail_scratch(&a.tail_ws, static_cast<size_t>(r) * tail_parts(r, pairs) * 256 * 256, s));
       }
     }
   }
-  CKS(streamk_scratch(&a.sk_ws, &a.sk_flags, &a.epoch));
+  CKS(streamk_scratch(&a.sk_ws, &a.sk_flags, &a.epoch, s));
   CK(launch_chain(kern, dim3(2 * pairs), dim3(kGemmThreads), Cfg::kSmemBytes, s, 2, ta, tb_half, a));
   if constexpr (EPI == kEpiSwiglu) {
     if (a.whole_tiles == 2) {
@@ -1323,7 +1330,9 @@ int cake_model_destroy(cake_model* m) {
   return CAKE_OK;
 }
 
-int cake_model_create(const cake_model_config* cfg, cake_model** out) {
+int cake_model_create(const cake_model_config* cfg, cake_model** out) { return cake_model_create_shared(cfg, nullptr, out); }
+
+int cake_model_create_shared(const cake_model_config* cfg, const cake_model* parent, cake_model** out) {
   *out = nullptr;
   const cake_model_config& c = *cfg;
   if (c.n_layers < 1 || c.hidden < 64 || c.n_heads < 1 || c.n_kv_heads < 1 || c.vocab < 1)
@@ -1364,72 +1373,87 @@ int cake_model_create(const cake_model_config* cfg, cake_model** out) {
     return code;
   };
 
-  // ---- weights (one arena, every tensor 128-B aligned)
   const size_t H = m->H, F = m->F, hd = m->hd, V = c.vocab;
-  auto pad = [](size_t n) { return (n + 63) / 64 * 64; };
-  const size_t per_layer =
-      pad(m->qkv_rows * H) + pad(H * m->nq * hd) + pad(2 * F * H) + pad(H * F) + 2 * pad(H);
-  m->weight_bytes = (per_layer * m->L + 2 * pad(V * H) + pad(H)) * sizeof(bf16);
-  if ((st = alloc_dev(&m->weight_arena, m->weight_bytes))) return bail(st);
-  bf16* w = static_cast<bf16*>(m->weight_arena);
-  auto take = [&](size_t n) {
-    bf16* p = w;
-    w += pad(n);
-    return p;
-  };
-  const uint64_t seed = c.seed;
-  const int r = c.tp_rank;
-  const float s_h = 1.0f / std::sqrt(static_cast<float>(c.hidden));
-  const float s_o = 1.0f / std::sqrt(static_cast<float>(c.n_heads * c.head_dim));
-  const float s_f = 1.0f / std::sqrt(static_cast<float>(c.ffn));
-  m->layers.resize(m->L);
-  for (int l = 0; l < m->L; ++l) {
-    LayerWeights& lw = m->layers[l];
-    lw.wqkv = take(m->qkv_rows * H);
-    lw.wo = take(H * m->nq * hd);
-    lw.wgu = take(2 * F * H);
-    lw.wd = take(H * F);
-    lw.ln1 = take(H);
-    lw.ln2 = take(H);
-    const long long qrows = static_cast<long long>(m->nq) * hd, kvrows = static_cast<long long>(m->nkv) * hd;
-    // QKV rows in rope-unit order within each head (qkv_row_of, elementwise.cuh)
-    if ((st = init_tensor(lw.wqkv, qrows, H, r * qrows, 0, H, 0, 0, seed, tid_layer(l, kWq), s_h, s, hd)))
-      return bail(st);
-    if ((st = init_tensor(lw.wqkv + qrows * H, kvrows, H, r * kvrows, 0, H, 0, 0, seed, tid_layer(l, kWk), s_h, s,
-                          hd)))
-      return bail(st);
-    if ((st = init_tensor(lw.wqkv + (qrows + kvrows) * H, kvrows, H, r * kvrows, 0, H, 0, 0, seed,
-                          tid_layer(l, kWv), s_h, s, hd)))
-      return bail(st);
-    if ((st = init_tensor(lw.wo, H, m->nq * hd, 0, r * qrows, c.n_heads * hd, 0, 0, seed, tid_layer(l, kWo), s_o, s)))
-      return bail(st);
-    // gate|up interleave: physical 256-row block b = [gate rows b*128..+128 | up rows b*128..+128]
-    for (long long b = 0; b < static_cast<long long>(F) / 128; ++b) {
-      if ((st = init_tensor(lw.wgu + (2 * b) * 128 * H, 128, H, r * F + b * 128, 0, H, 0, 0, seed,
-                            tid_layer(l, kWgate), s_h, s)))
+  if (parent != nullptr) {
+    // ---- weights shared with `parent` (a concurrent request's context on the same
+    // device): the sibling owns its pool, scratch and tensor maps over them only
+    const cake_model_config& pc = parent->cfg;
+    if (pc.n_layers != c.n_layers || pc.hidden != c.hidden || pc.n_heads != c.n_heads ||
+        pc.n_kv_heads != c.n_kv_heads || pc.head_dim != c.head_dim || pc.ffn != c.ffn || pc.vocab != c.vocab ||
+        pc.seed != c.seed || pc.tp_rank != c.tp_rank || pc.tp_size != c.tp_size)
+      return bail(fail(CAKE_EINVAL, "model: shared weights need the same dimensions, seed and TP shard"));
+    m->layers = parent->layers;  // device pointers + weight tensor maps
+    m->embed = parent->embed;
+    m->lm_head = parent->lm_head;
+    m->final_norm = parent->final_norm;
+    m->weight_bytes = 0;
+  } else {
+    // ---- weights (one arena, every tensor 128-B aligned)
+    auto pad = [](size_t n) { return (n + 63) / 64 * 64; };
+    const size_t per_layer =
+        pad(m->qkv_rows * H) + pad(H * m->nq * hd) + pad(2 * F * H) + pad(H * F) + 2 * pad(H);
+    m->weight_bytes = (per_layer * m->L + 2 * pad(V * H) + pad(H)) * sizeof(bf16);
+    if ((st = alloc_dev(&m->weight_arena, m->weight_bytes))) return bail(st);
+    bf16* w = static_cast<bf16*>(m->weight_arena);
+    auto take = [&](size_t n) {
+      bf16* p = w;
+      w += pad(n);
+      return p;
+    };
+    const uint64_t seed = c.seed;
+    const int r = c.tp_rank;
+    const float s_h = 1.0f / std::sqrt(static_cast<float>(c.hidden));
+    const float s_o = 1.0f / std::sqrt(static_cast<float>(c.n_heads * c.head_dim));
+    const float s_f = 1.0f / std::sqrt(static_cast<float>(c.ffn));
+    m->layers.resize(m->L);
+    for (int l = 0; l < m->L; ++l) {
+      LayerWeights& lw = m->layers[l];
+      lw.wqkv = take(m->qkv_rows * H);
+      lw.wo = take(H * m->nq * hd);
+      lw.wgu = take(2 * F * H);
+      lw.wd = take(H * F);
+      lw.ln1 = take(H);
+      lw.ln2 = take(H);
+      const long long qrows = static_cast<long long>(m->nq) * hd, kvrows = static_cast<long long>(m->nkv) * hd;
+      // QKV rows in rope-unit order within each head (qkv_row_of, elementwise.cuh)
+      if ((st = init_tensor(lw.wqkv, qrows, H, r * qrows, 0, H, 0, 0, seed, tid_layer(l, kWq), s_h, s, hd)))
         return bail(st);
-      if ((st = init_tensor(lw.wgu + (2 * b + 1) * 128 * H, 128, H, r * F + b * 128, 0, H, 0, 0, seed,
-                            tid_layer(l, kWup), s_h, s)))
+      if ((st = init_tensor(lw.wqkv + qrows * H, kvrows, H, r * kvrows, 0, H, 0, 0, seed, tid_layer(l, kWk), s_h, s,
+                            hd)))
         return bail(st);
+      if ((st = init_tensor(lw.wqkv + (qrows + kvrows) * H, kvrows, H, r * kvrows, 0, H, 0, 0, seed,
+                            tid_layer(l, kWv), s_h, s, hd)))
+        return bail(st);
+      if ((st = init_tensor(lw.wo, H, m->nq * hd, 0, r * qrows, c.n_heads * hd, 0, 0, seed, tid_layer(l, kWo), s_o, s)))
+        return bail(st);
+      // gate|up interleave: physical 256-row block b = [gate rows b*128..+128 | up rows b*128..+128]
+      for (long long b = 0; b < static_cast<long long>(F) / 128; ++b) {
+        if ((st = init_tensor(lw.wgu + (2 * b) * 128 * H, 128, H, r * F + b * 128, 0, H, 0, 0, seed,
+                              tid_layer(l, kWgate), s_h, s)))
+          return bail(st);
+        if ((st = init_tensor(lw.wgu + (2 * b + 1) * 128 * H, 128, H, r * F + b * 128, 0, H, 0, 0, seed,
+                              tid_layer(l, kWup), s_h, s)))
+          return bail(st);
+      }
+      if ((st = init_tensor(lw.wd, H, F, 0, r * F, c.ffn, 0, 0, seed, tid_layer(l, kWdown), s_f, s))) return bail(st);
+      if ((st = fill(lw.ln1, H, 1.0f, s))) return bail(st);
+      if ((st = fill(lw.ln2, H, 1.0f, s))) return bail(st);
+      for (int ci = 0; ci < 3; ++ci) {
+        const uint32_t div = 1u << ci;  // cluster size 1, 2, 4
+        if ((st = make_map(&lw.m_qkv[ci], lw.wqkv, m->qkv_rows, H, m->bn_qkv / div))) return bail(st);
+        if (m->qkv_rows % 192 == 0 && (st = make_map(&lw.m_qkv192[ci], lw.wqkv, m->qkv_rows, H, 96))) return bail(st);
+        if ((st = make_map(&lw.m_o[ci], lw.wo, H, m->nq * hd, 128 / div))) return bail(st);
+        if ((st = make_map(&lw.m_gu[ci], lw.wgu, 2 * F, H, 256 / div))) return bail(st);
+        if ((st = make_map(&lw.m_d[ci], lw.wd, H, F, 128 / div))) return bail(st);
+      }
     }
-    if ((st = init_tensor(lw.wd, H, F, 0, r * F, c.ffn, 0, 0, seed, tid_layer(l, kWdown), s_f, s))) return bail(st);
-    if ((st = fill(lw.ln1, H, 1.0f, s))) return bail(st);
-    if ((st = fill(lw.ln2, H, 1.0f, s))) return bail(st);
-    for (int ci = 0; ci < 3; ++ci) {
-      const uint32_t div = 1u << ci;  // cluster size 1, 2, 4
-      if ((st = make_map(&lw.m_qkv[ci], lw.wqkv, m->qkv_rows, H, m->bn_qkv / div))) return bail(st);
-      if (m->qkv_rows % 192 == 0 && (st = make_map(&lw.m_qkv192[ci], lw.wqkv, m->qkv_rows, H, 96))) return bail(st);
-      if ((st = make_map(&lw.m_o[ci], lw.wo, H, m->nq * hd, 128 / div))) return bail(st);
-      if ((st = make_map(&lw.m_gu[ci], lw.wgu, 2 * F, H, 256 / div))) return bail(st);
-      if ((st = make_map(&lw.m_d[ci], lw.wd, H, F, 128 / div))) return bail(st);
-    }
+    m->embed = take(V * H);
+    m->lm_head = take(V * H);
+    m->final_norm = take(H);
+    if ((st = init_tensor(m->embed, V, H, 0, 0, H, 0, 0, seed, kTidEmbed, 1.0f, s))) return bail(st);
+    if ((st = init_tensor(m->lm_head, V, H, 0, 0, H, 0, 0, seed, kTidLmHead, s_h, s))) return bail(st);
+    if ((st = fill(m->final_norm, H, 1.0f, s))) return bail(st);
   }
-  m->embed = take(V * H);
-  m->lm_head = take(V * H);
-  m->final_norm = take(H);
-  if ((st = init_tensor(m->embed, V, H, 0, 0, H, 0, 0, seed, kTidEmbed, 1.0f, s))) return bail(st);
-  if ((st = init_tensor(m->lm_head, V, H, 0, 0, H, 0, 0, seed, kTidLmHead, s_h, s))) return bail(st);
-  if ((st = fill(m->final_norm, H, 1.0f, s))) return bail(st);
 
   // ---- paged KV pool
   m->n_logical_pages = static_cast<int>((c.max_tokens + c.page_tokens - 1) / c.page_tokens);

@@ -55,6 +55,14 @@ BandwidthTrace to_trace(const cake_trace& t) {
   return BandwidthTrace(std::move(pts));
 }
 
+#ifndef CAKE_REFERENCE_BUILD
+}  // namespace
+struct cake_link {
+  std::shared_ptr<SharedLink> link;
+};
+namespace {
+#endif
+
 RunOptions to_opts(const cake_run_opts* o) {
   RunOptions r;
   if (!o) return r;
@@ -71,7 +79,9 @@ RunOptions to_opts(const cake_run_opts* o) {
   r.cached_prefix = o->cached_prefix != 0;
   r.race_force = o->race_force;
   r.race_hold = o->race_hold;
+  if (o->link) r.link = static_cast<const cake_link*>(o->link)->link;
 #else
+  if (o->link) throw std::invalid_argument("link is a B200 extension");
   if (o->race_to_finish) throw std::invalid_argument("race_to_finish is a B200 extension");
   if (o->cached_prefix) throw std::invalid_argument("cached_prefix is a B200 extension");
 #endif
@@ -140,7 +150,9 @@ struct cake_store {
 struct cake_gpu {
   std::unique_ptr<GpuContext> ctx;
   Codec codec = Codec::identity();  // cache-tier codec of build_tier and run
+  std::shared_ptr<SharedLink> link;  // set: runs pace through this shared link
 };
+
 #endif
 
 extern "C" {
@@ -401,10 +413,39 @@ int cake_gpu_create(const cake_gpu_config* c, cake_gpu** out) {
     if (c->race_margin_us > 0) o.race_margin_us = c->race_margin_us;
     if (c->tp_shm) o.tp_shm = c->tp_shm;
     o.compute_sms = c->compute_sms;
+    if (c->weights_from) o.weights_from = c->weights_from->ctx.get();
     auto g = std::make_unique<cake_gpu>();
     g->ctx = std::make_unique<GpuContext>(m, o);
     *out = g.release();
   });
+}
+
+int cake_link_create(cake_trace trace, cake_link** out) {
+  return guarded([&] {
+    auto l = std::make_unique<cake_link>();
+    l->link = std::make_shared<SharedLink>(to_trace(trace));
+    *out = l.release();
+  });
+}
+
+int cake_link_destroy(cake_link* l) {
+  delete l;
+  return CAKE_OK;
+}
+
+int cake_link_reset(cake_link* l) {
+  return guarded([&] { l->link->reset(); });
+}
+
+int cake_link_reserved_bits(const cake_link* l, uint64_t* bits, int64_t* now_us) {
+  return guarded([&] {
+    *bits = l->link->reserved_bits();
+    if (now_us) *now_us = l->link->timer().now_us();
+  });
+}
+
+int cake_gpu_set_link(cake_gpu* g, cake_link* l) {
+  return guarded([&] { g->link = l ? l->link : nullptr; });
 }
 
 int cake_gpu_destroy(cake_gpu* g) {
@@ -452,6 +493,7 @@ int cake_gpu_run(cake_gpu* g, cake_store* s, uint64_t total_tokens, uint32_t chu
     req.chunk_size = chunk_size;
     RunOptions o = to_opts(opts);
     o.gpu = g->ctx.get();
+    if (!o.link) o.link = g->link;
     const GpuModelConfig& mc = g->ctx->config();
     const ModelProfile prof = mc.profile(g->ctx->options().tp_size);
     const RunReport r = run(req, prof, g->ctx->options().prior, to_trace(trace), g->codec, to_mode(mode),

@@ -200,7 +200,9 @@ GpuContext::GpuContext(const GpuModelConfig& cfg, const GpuOptions& opt) : impl_
   g.ev_final_start = std::make_unique<Event>();
   g.ev_logits = std::make_unique<Event>();
   g.ev_reset = std::make_unique<Event>();
-  check(cake_model_create(&mc, &g.model), "model create");
+  check(opt.weights_from ? cake_model_create_shared(&mc, opt.weights_from->model(), &g.model)
+                         : cake_model_create(&mc, &g.model),
+        "model create");
   check(cake_model_get_info(g.model, &g.info), "model info");
   // tp_size > 1 without a communicator is allowed for the single-device
   // group driver (cake_prefill_group); a live run then fails loudly in the
@@ -275,6 +277,12 @@ void check_chunking(const GpuContext::Impl& g, std::span<const ChunkSpec> chunks
       throw std::invalid_argument("gpu: chunk_size must be a multiple of page_tokens (" +
                                   std::to_string(g.cfg.page_tokens) + ")");
   }
+}
+
+// Drain this context's streams only: another context on the same device
+// (a concurrent request) keeps running.
+void sync_own_streams(GpuContext::Impl& g) {
+  for (void* s : {g.s_compute, g.s_copy, g.s_control}) check(cake_stream_sync(s), "pre-run sync");
 }
 
 void upload_tokens(GpuContext::Impl& g, const std::vector<std::uint32_t>& ids, void* stream) {
@@ -383,7 +391,7 @@ CostModel GpuContext::calibrate(const RequestSpec& request, std::uint64_t prompt
 
 void GpuContext::poison(int byte) {
   Impl& g = *impl_;
-  check(cake_cuda_device_sync(), "poison: drain");
+  sync_own_streams(g);  // (not the device: another context may be running)
   check(cake_kv_poison(g.model, byte, g.s_compute), "poison pool");
   for (auto& s : g.staging) check(cake_memset_async(s.p, byte & 0xFF, g.staging_bytes, g.s_compute), "poison staging");
   check(cake_stream_sync(g.s_compute), "poison: sync");
@@ -675,7 +683,7 @@ RunReport run_follower(GpuContext::Impl& g, TpCoordinator& tp, const RunPlan& pl
   const auto n = static_cast<std::uint32_t>(plan.chunks.size());
   g.ensure_events(n);
   tp.begin_run(++g.run_counter, n);
-  check(cake_cuda_device_sync(), "pre-run sync");
+  sync_own_streams(g);
   RunTimer timer;
   check(cake_event_record(g.ev_anchor->h, g.s_compute), "anchor");
   const Micros t0 = timer.now_us();
@@ -800,7 +808,7 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   const bool race = opt.race_to_finish && io_on && compute_on && tp == nullptr;  // TP: boundary race not mirrored yet
   g.ensure_events(n_all);
   if (tp) tp->begin_run(++g.run_counter, n);
-  check(cake_cuda_device_sync(), "pre-run sync");
+  sync_own_streams(g);
   long long launches0 = 0;
   check(cake_model_launch_count(g.model, &launches0, 1), "launch count");
 
@@ -831,6 +839,7 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
     t.jitter_seed = opt.jitter_seed;
     t.record_slices = opt.record_slices;
     t.sink = &sink;
+    t.link = opt.link;
     if (race) {
       t.contest = [&](const FetchTask& task, Micros io_eta) {
         if (opt.race_force == 1) return false;

@@ -33,7 +33,7 @@ class CakeRunOpts(C.Structure):
     _fields_ = [("compute_enabled", C.c_int), ("io_enabled", C.c_int), ("token_budget", u32),
                 ("throttle_quantum_bytes", u64), ("decode_us_per_byte", dbl), ("jitter_max_us", u32),
                 ("jitter_seed", u64), ("race_to_finish", C.c_int), ("cached_prefix", C.c_int),
-                ("record_slices", C.c_int), ("race_force", C.c_int), ("race_hold", C.c_int)]
+                ("record_slices", C.c_int), ("race_force", C.c_int), ("race_hold", C.c_int), ("link", vp)]
 
 
 class CakeSummary(C.Structure):
@@ -47,7 +47,8 @@ class CakeGpuConfig(C.Structure):
                 ("rms_eps", C.c_float), ("max_chunk", C.c_int), ("max_tokens", C.c_longlong),
                 ("weight_seed", C.c_ulonglong), ("device", C.c_int), ("tp_rank", C.c_int), ("tp_size", C.c_int),
                 ("nccl_comm", vp), ("lookahead_layers", C.c_int), ("profile_kernels", C.c_int),
-                ("race_margin_us", i64), ("tp_shm", C.c_char_p), ("compute_sms", C.c_int)]
+                ("race_margin_us", i64), ("tp_shm", C.c_char_p), ("compute_sms", C.c_int),
+                ("weights_from", vp)]
 
 
 class CakeGpuResult(C.Structure):
@@ -95,6 +96,11 @@ _SIGS = {
     "cake_run_store": (C.c_int, [vp, u64, u32, u32, u32, u32, C.c_char_p, dbl, dbl, u32, CakeTrace, C.c_int,
                                  C.c_int, u64, dbl, P(CakeRunOpts), P(CakeSummary), P(CakeRecord)]),
     "cake_gpu_create": (C.c_int, [P(CakeGpuConfig), P(vp)]),
+    "cake_link_create": (C.c_int, [CakeTrace, P(vp)]),
+    "cake_link_destroy": (C.c_int, [vp]),
+    "cake_link_reset": (C.c_int, [vp]),
+    "cake_link_reserved_bits": (C.c_int, [vp, P(u64), P(i64)]),
+    "cake_gpu_set_link": (C.c_int, [vp, vp]),
     "cake_gpu_destroy": (C.c_int, [vp]),
     "cake_gpu_kv_bytes_per_token": (C.c_int, [vp, P(u64)]),
     "cake_gpu_build_tier": (C.c_int, [vp, vp, u64, u32, u64]),

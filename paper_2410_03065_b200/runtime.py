@@ -46,12 +46,46 @@ class GpuResult:
     chunks: list = field(default_factory=list)
 
 
+class Link:
+    """One emulated cache-tier link shared by several GpuRuntimes (concurrent
+    requests on one device): together their loaders deliver at the trace rate;
+    the trace's time axis is the link's clock (t = 0 at creation / reset())."""
+
+    def __init__(self, trace: BandwidthTrace | None = None, *, mbps: float | None = None):
+        self.n = N.load()
+        trace = trace or BandwidthTrace.constant(mbps)
+        t, self._keep = trace.native()
+        h = N.vp()
+        self.n.call("cake_link_create", t, C.byref(h))
+        self.h = h.value
+
+    def reset(self):
+        self.n.call("cake_link_reset", self.h)
+
+    def reserved(self) -> tuple[int, int]:
+        """(bits reserved so far, link clock in us)."""
+        b, t = N.u64(), N.i64()
+        self.n.call("cake_link_reserved_bits", self.h, C.byref(b), C.byref(t))
+        return b.value, t.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.n.lib.cake_link_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class GpuRuntime:
     def __init__(self, preset, *, n_layers: int | None = None, max_chunk: int = 512, max_tokens: int = 32768,
                  weight_seed: int = 1234, device: int = 0, tp_rank: int = 0, tp_size: int = 1, nccl_comm=None,
                  lookahead_layers: int = 0, profile_kernels: bool = False, race_margin_us: int = 0,
                  rope_theta: float = 500000.0, rms_eps: float = 1e-5, tp_shm: str | None = None,
-                 compute_sms: int = 0):
+                 compute_sms: int = 0, weights_from: "GpuRuntime | None" = None):
         self.n = N.load()
         dims = PRESETS[preset] if isinstance(preset, str) else tuple(preset)
         L, H, nh, nkv, hd, ffn, vocab = dims
@@ -61,12 +95,15 @@ class GpuRuntime:
         cfg = N.CakeGpuConfig(L, H, nh, nkv, hd, ffn, vocab, rope_theta, rms_eps, max_chunk, max_tokens,
                               weight_seed, device, tp_rank, tp_size, nccl_comm, lookahead_layers,
                               1 if profile_kernels else 0, race_margin_us,
-                              tp_shm.encode() if tp_shm else None, compute_sms)
+                              tp_shm.encode() if tp_shm else None, compute_sms,
+                              weights_from.h if weights_from is not None else None)
         h = N.vp()
         self.n.call("cake_gpu_create", C.byref(cfg), C.byref(h))
         self.h = h.value
         self.vocab = vocab
         self.max_chunk = max_chunk
+        self._parent = weights_from  # shared weights: the parent context must outlive this one
+        self._link = None
 
     def close(self):
         if getattr(self, "h", None):
@@ -78,6 +115,12 @@ class GpuRuntime:
             self.close()
         except Exception:
             pass
+
+    def attach_link(self, link: "Link | None"):
+        """Pace later runs' loads through `link` (shared with other contexts) instead of
+        their own trace; None detaches."""
+        self.n.call("cake_gpu_set_link", self.h, link.h if link is not None else None)
+        self._link = link
 
     @property
     def kv_bytes_per_token(self) -> int:
