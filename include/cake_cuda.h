@@ -238,8 +238,11 @@ CAKE_API int cake_gemm_set_schedule(int schedule);
  * projections; ATTN_MAX_WAVES = CTA waves the split-KV dispatch may use (1);
  * GEMM_NOSPLIT 1 = no split-K for the few-tile pair GEMMs (0). */
 enum { CAKE_EXP_PDL = 0, CAKE_EXP_FUSED_NORM = 1, CAKE_EXP_ATTN_MAX_WAVES = 2, CAKE_EXP_GEMM_NOSPLIT = 3,
-       CAKE_EXP_COUNT = 4 };
+       CAKE_EXP_DEC_CHAIN = 4, /* 1: first-token projections on the persistent chain kernel, 0: per-projection GEMVs */
+       CAKE_EXP_COUNT = 5 };
 CAKE_API int cake_set_experiment(int knob, int value);
+/* First-token chain kernel: L2 prefetch per CTA ahead of each phase, in KB (A/B; default 128). */
+CAKE_API int cake_dec_set_prefetch(int kb);
 /* C = A · B^T for bf16 row-major A [M, K], B [N, K]; epi 0: bf16 C, 1: fp32 C,
  * 2: fp32 C += . block_n 128 or 256. For tests and microbenchmarks. */
 CAKE_API int cake_gemm(const void* dA, const void* dB, void* dC, int M, int N, int K, int epi, int block_n,

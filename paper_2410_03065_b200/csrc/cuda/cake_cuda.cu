@@ -29,6 +29,7 @@
 #include "gemm2.cuh"
 #include "gemm2c.cuh"
 #include "skinny.cuh"
+#include "decode_chain.cuh"
 
 using namespace cake_dev;
 using bf16 = __nv_bfloat16;
@@ -76,7 +77,7 @@ cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 // the next kernel's CTAs become resident and run their prologue (barrier
 // init, TMEM alloc, descriptor prefetch) while the previous kernel drains.
 // A/B switches for measurements (cake_set_experiment); the defaults are the product.
-int g_exp[CAKE_EXP_COUNT] = {1 /*PDL*/, 1 /*FUSED_NORM*/, 1 /*ATTN_MAX_WAVES*/, 0 /*GEMM_NOSPLIT*/};
+int g_exp[CAKE_EXP_COUNT] = {1 /*PDL*/, 1 /*FUSED_NORM*/, 1 /*ATTN_MAX_WAVES*/, 0 /*GEMM_NOSPLIT*/, 1 /*DEC_CHAIN*/};
 
 // cake_set_experiment(CAKE_EXP_PDL, 0) turns programmatic dependent launch off.
 bool pdl_enabled() { return g_exp[CAKE_EXP_PDL] != 0; }
@@ -579,6 +580,7 @@ struct cake_model {
   float* tp_buf = nullptr;  // fp32 partial sums for the TP all-reduce
   float* ss = nullptr;      // fused RMSNorm: [H / 128][rows_cap] partial sums of squares of the residual rows
   unsigned* q8_ws = nullptr;  // quant8 encode: ordered min/max keys
+  unsigned* dec_bar = nullptr;  // first-token chain kernel: grid barrier (arrivals, generation)
   CUtensorMap a_xn[3], a_attn[3], a_act[3];
   CUtensorMap out_h[2];  // staged residual epilogue: h (fp32, 32-col boxes), xn = bf16(h) (64-col boxes)  // activation maps, boxes of 128 / 64 / 32 rows (gemm2c pieces)
   CUtensorMap tm_q, tm_kv;  // attention: Q rows of a GQA group, paged K/V pool
@@ -952,9 +954,93 @@ int skinny_row_parallel(cake_model* m, int kind, const bf16* W, const bf16* x, i
 
 int rmsnorm(cake_model* m, const bf16* gamma, long long row0, int rows, const int32_t* abort_flag, cudaStream_t s);
 
+// One launch of the first-token projection chain (decode_chain.cuh): the o,
+// gate/up and down projections of `layer` (layer >= 0) and then the q
+// projection of `q_layer` (q_layer >= 0), one CTA per SM, grid barriers
+// between the phases. Cooperative launch: every CTA is resident before any
+// spins in a barrier (two contexts' chains never split the SMs between them).
+int g_dec_prefetch_kb = 128;  // L2 prefetch per CTA ahead of each chain phase (A/B: cake_dec_set_prefetch)
+int dec_chain(cake_model* m, int layer, int q_layer, long long pos, cudaStream_t s) {
+  DecArgs a{};
+  auto add = [&](int kind, const bf16* W, const bf16* gamma, int K, int units) {
+    a.ph[a.n_phases++] = DecPhase{kind, W, gamma, K, units};
+  };
+  if (layer >= 0) {
+    const LayerWeights& lw = m->layers[layer];
+    add(kDecO, lw.wo, nullptr, m->nq * m->hd, m->H);
+    add(kDecGU, lw.wgu, lw.ln2, m->H, m->F);
+    add(kDecD, lw.wd, nullptr, m->F, m->H);
+  }
+  if (q_layer >= 0) add(kDecQ, m->layers[q_layer].wqkv, m->layers[q_layer].ln1, m->H, m->nq * m->hd / 2);
+  double bytes = 0.0;
+  const int ctas = num_sms();
+  for (int p = 0; p < a.n_phases; ++p) {
+    const int rpu = (a.ph[p].kind == kDecQ || a.ph[p].kind == kDecGU) ? 2 : 1;
+    a.max_k = std::max(a.max_k, a.ph[p].K);
+    a.red_rows = std::max(a.red_rows, rpu * ((a.ph[p].units + ctas - 1) / ctas));
+    bytes += 2.0 * rpu * a.ph[p].K * a.ph[p].units;
+    if (a.ph[p].K % 8) return fail(CAKE_EINVAL, "decode chain: row length %d not a multiple of 8", a.ph[p].K);
+  }
+  a.prefetch_bytes = g_dec_prefetch_kb * 1024;
+  a.h = m->h;
+  a.H = m->H;
+  a.eps = m->cfg.rms_eps;
+  a.attn = m->attn;
+  a.act = m->act;
+  a.q_out = m->q;
+  a.rope = m->rope;
+  a.pos = pos;
+  a.head_dim = m->hd;
+  a.gbar = m->dec_bar;
+  const size_t smem = static_cast<size_t>(a.max_k) * 2 + sizeof(float) * a.red_rows;
+  static bool cfgd = false;
+  if (!cfgd) {
+    CK(cudaFuncSetAttribute(dec_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    cfgd = true;
+  }
+  if (smem > 200 * 1024) return fail(CAKE_EINVAL, "decode chain: %zu B of shared memory", smem);
+  ProfScope ps(m, CAKE_K_DEC_PROJ, s, bytes, bytes);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  attr[n].id = cudaLaunchAttributeCooperative;
+  attr[n].val.cooperative = 1;
+  ++n;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(kDecThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  CK(cudaLaunchKernelEx(&cfg, dec_chain_kernel, a));
+  return CAKE_OK;
+}
+
+// First-token step on the chain kernel: embed, then per layer the attention
+// between two chain launches (q(0) | attn(0) | o,gu,down(0) + q(1) | attn(1) | ...).
+int last_token_chain(cake_model* m, const int32_t* d_token, long long T, const int32_t* bt, cudaStream_t s) {
+  {
+    ProfScope ps(m, CAKE_K_EMBED, s, 0.0, m->H * 6.0);
+    embed_kernel<<<1, 128, 0, s>>>(d_token, m->embed, m->h, m->H, nullptr);
+    CKL();
+  }
+  CKS(dec_chain(m, -1, 0, T - 1, s));
+  for (int l = 0; l < m->L; ++l) {
+    CKS(attention(m, T - 1, 1, l, bt, nullptr, s));
+    CKS(dec_chain(m, l, l + 1 < m->L ? l + 1 : -1, T - 1, s));
+  }
+  return CAKE_OK;
+}
+
 // First-token step over a complete cache: the last prompt token (position
 // T-1) as a q-only pass, every projection a weight stream.
 int last_token_pass(cake_model* m, const int32_t* d_token, long long T, const int32_t* bt, cudaStream_t s) {
+  if (m->cfg.tp_size == 1 && !m->emulated_tp && g_exp[CAKE_EXP_DEC_CHAIN]) return last_token_chain(m, d_token, T, bt, s);
   const int H = m->H;
   {
     ProfScope ps(m, CAKE_K_EMBED, s, 0.0, H * 6.0);
@@ -1319,6 +1405,7 @@ int cake_model_destroy(cake_model* m) {
                   static_cast<void*>(m->q), static_cast<void*>(m->attn), static_cast<void*>(m->act),
                   static_cast<void*>(m->part_o), static_cast<void*>(m->part_lse),
                   static_cast<void*>(m->tp_buf), static_cast<void*>(m->q8_ws), static_cast<void*>(m->ss),
+                  static_cast<void*>(m->dec_bar),
                   static_cast<void*>(m->attn_tickets)})
     if (p) cudaFree(p);
   for (auto& p : m->prof) {
@@ -1501,6 +1588,8 @@ int cake_model_create_shared(const cake_model_config* cfg, const cake_model* par
   if (c.tp_size > 1 && (st = alloc_dev(reinterpret_cast<void**>(&m->tp_buf), R * H * sizeof(float))))
     return bail(st);
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->q8_ws), 2 * sizeof(unsigned)))) return bail(st);
+  if ((st = alloc_dev(reinterpret_cast<void**>(&m->dec_bar), 2 * sizeof(unsigned)))) return bail(st);
+  cudaMemset(m->dec_bar, 0, 2 * sizeof(unsigned));
   cudaMemset(m->xn, 0, R * H * sizeof(bf16));
   cudaMemset(m->attn, 0, R * m->nq * hd * sizeof(bf16));
   cudaMemset(m->act, 0, R * F * sizeof(bf16));
@@ -1822,6 +1911,12 @@ int cake_gemm_set_schedule(int schedule) {
   g_gemm_schedule = schedule & 1;
   g_gemm_2sm = (schedule & 2) ? 0 : 1;
   g_gemm_cluster = (schedule & 4) ? 1 : 0;
+  return CAKE_OK;
+}
+
+int cake_dec_set_prefetch(int kb) {
+  if (kb < 0) return fail(CAKE_EINVAL, "dec prefetch: kb >= 0");
+  g_dec_prefetch_kb = kb;
   return CAKE_OK;
 }
 

@@ -19,15 +19,19 @@ REPS = int(os.environ.get("REPS", "20"))
 preset = os.environ.get("PRESET", "llama3_8b")
 rt = GpuRuntime(preset, max_tokens=T, max_chunk=512)
 tier = rt.build_cache_tier(T, 512, 42)
-r = rt.run(tier, T, 512, 42, mbps=256000, mode="io_only")
-print(f"run: final step {r.final_step_ms:.3f} ms (in situ)", flush=True)
 lib = native.load()
 lib.lib.cake_gpu_model.restype = ctypes.c_void_p
 lib.lib.cake_gpu_model.argtypes = [ctypes.c_void_p]
 model = lib.lib.cake_gpu_model(rt.h)
 cl = native.load_cuda()
+if os.environ.get("PREFETCH_KB") is not None:
+    cl.cake_dec_set_prefetch(int(os.environ["PREFETCH_KB"]))
+if os.environ.get("CHAIN") is not None:
+    cl.cake_set_experiment(4, int(os.environ["CHAIN"]))  # CAKE_EXP_DEC_CHAIN
 cl.cake_final_logits.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+r = rt.run(tier, T, 512, 42, mbps=256000, mode="io_only")
+print(f"run: final step {r.final_step_ms:.3f} ms (in situ)", flush=True)
 V = rt.vocab
 tok = torch.tensor([7], dtype=torch.int32, device="cuda")
 bt = torch.arange((T + 63) // 64, dtype=torch.int32, device="cuda")
