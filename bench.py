@@ -184,6 +184,47 @@ def cpu_baseline(T, C, mbps, budget_s=20.0):
     }
 
 
+def config1_live_cpu(mbps=800.0, modes=("cake", "compute_only", "io_only")):
+    """BASELINE config 1 served for real on the host cores, nothing extrapolated:
+    the reference's own live run (oracle/_ref/ref_live_cpu: its scheduler, loader and
+    store sources) with its compute sleep replaced by the CPU forward (llama_ref.c)."""
+    import tempfile
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_live_cpu")
+    if not os.path.exists(exe):
+        return None
+    threads = max(1, (os.cpu_count() or 2) - 2)  # two cores stay with the loader's reader and pacer
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        for mode in modes:
+            p = subprocess.run([exe, "2048", "256", str(mbps), str(threads), os.path.join(d, mode), mode],
+                               capture_output=True, text=True, timeout=600)
+            if p.returncode != 0:
+                return {"error": p.stderr[-300:]}
+            out[mode] = json.loads(p.stdout)
+    return out
+
+
+def config1_gpu(mbps=800.0, reps=5):
+    """The same config-1 request on the GPU path (tiny preset, file-free pinned tier)."""
+    from paper_2410_03065_b200.runtime import GpuRuntime
+
+    rt = GpuRuntime("tiny", max_tokens=2048, max_chunk=256)
+    try:
+        tier = rt.build_cache_tier(2048, 256, 42)
+        out = {}
+        for mode in ("cake", "compute_only", "io_only"):
+            rs = [rt.run(tier, 2048, 256, 42, mbps=mbps, mode=mode) for _ in range(reps + 1)][1:]
+            best = min(rs, key=lambda r: r.first_token_ms)
+            out[mode] = {"first_token_ms": best.first_token_ms, "device_ttft_ms": best.device_ttft_ms,
+                         "ttft_ms": best.kv_resident_ms, "merge_point": best.merge_point,
+                         "top1": int(rt.logits().argmax()) if mode == "io_only" else None}
+        tier.close()
+        return out
+    finally:
+        rt.close()
+
+
 # ------------------------------------------------------------------ arms
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
@@ -207,7 +248,8 @@ def reference_arm(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(workload_config(args.tokens, args.chunk, args.mbps, 1),
                            parallelism=f"host CPU, {last['cores']} threads (reference scheduler + CPU Llama forward)"),
-            "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": dict({k: last[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                                 config1_live=config1_live_cpu()),
             "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -351,6 +393,10 @@ def b200_arm(args):
         try:
             line["cpu_baseline"] = {k: v for k, v in cpu_baseline(T, C, mbps).items()
                                     if k in ("value", "unit", "cores", "kind", "sample")}
+            # BASELINE config 1 end to end on both: the reference's live loop on the host
+            # cores (no extrapolation) next to the GPU path, same prompt and link
+            line["config1"] = {"workload": "tiny 2-layer d=256 4-head, T=2048 chunk=256, tier behind 800 mbps",
+                               "cpu_live": config1_live_cpu(), "gpu": config1_gpu()}
         except Exception as e:  # reported, never fatal to the GPU line
             line["cpu_baseline"] = {"value": None, "unit": "ms", "cores": os.cpu_count(), "kind": "reference",
                                     "sample": f"failed: {e}"}
