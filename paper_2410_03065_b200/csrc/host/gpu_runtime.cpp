@@ -15,6 +15,8 @@
 #include <stdexcept>
 #include <thread>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "cake/gpu.hpp"
 #include "cake_cuda.h"
 #include "internal.hpp"
@@ -22,6 +24,15 @@
 namespace cake {
 
 namespace {
+
+// NVTX annotations (header-only nvtx3: free unless a tool such as nsys is
+// attached): the per-chunk, per-side timeline the reference keeps as its event
+// CSV (proj/src/report.cpp:31-37), on the host threads that drive the GPU.
+struct NvtxScope {
+  explicit NvtxScope(const std::string& name) { nvtxRangePushA(name.c_str()); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+void nvtx_mark(const std::string& name) { nvtxMarkA(name.c_str()); }
 
 void check(int st, const char* what) {
   if (st == CAKE_OK) return;
@@ -465,6 +476,7 @@ struct LiveRun {
     }
     int expected = kNone;
     if (!commit[i].compare_exchange_strong(expected, who)) return false;
+    nvtx_mark("commit chunk " + std::to_string(i) + (who == kByCompute ? " by compute" : " by io"));
     {
       std::lock_guard lk(commit_mu);
       ++n_committed;
@@ -527,6 +539,7 @@ class GpuPrefillBackend final : public PrefillBackend {
 
   void launch(const ChunkSpec& c, bool contested) override {
     GpuContext::Impl& g = r_.g;
+    NvtxScope nv("compute chunk " + std::to_string(c.index) + (contested ? " (contested)" : ""));
     if (r_.tp) r_.tp->publish_compute(c.index);  // followers enqueue the same chunk (NCCL lockstep)
     const Micros predicted = predict_finish(c);
     if (contested) r_.start_race(c, kByCompute, g.s_compute);
@@ -617,8 +630,14 @@ class GpuLoaderSink final : public ChunkSink {
  public:
   GpuLoaderSink(LiveRun& run, bool q8) : r_(run), q8_(q8) {}
 
+  ~GpuLoaderSink() override {
+    if (range_) nvtxRangeEnd(range_);
+  }
+
   void begin_chunk(const FetchTask& t) override {
     GpuContext::Impl& g = r_.g;
+    if (range_) nvtxRangeEnd(range_);  // an abandoned chunk never reached end_chunk
+    range_ = nvtxRangeStartA(("load chunk " + std::to_string(t.chunk.index) + (t.contested ? " (contested)" : "")).c_str());
     if (r_.tp) r_.tp->publish_io(t.chunk.index);  // every rank loads its shard of this chunk
     if (t.contested) r_.start_race(t.chunk, kByIo, g.s_copy);
     // quant8: land the 4-B header at +12 so the level payload is 16-B aligned
@@ -643,6 +662,8 @@ class GpuLoaderSink final : public ChunkSink {
                             static_cast<long long>(t.encoded_bytes), g.s_copy),
             "scatter");
     check(cake_event_record(g.ev_io[t.chunk.index]->h, g.s_copy), "record");
+    nvtxRangeEnd(range_);
+    range_ = 0;
   }
 
   Micros wait_chunk(const FetchTask& t) override {
@@ -669,6 +690,7 @@ class GpuLoaderSink final : public ChunkSink {
   std::byte* buf_ = nullptr;
   int parity_ = 0;
   std::uint64_t h2d_bytes_ = 0;
+  nvtxRangeId_t range_ = 0;  // the chunk being paced (pacer thread only)
 };
 
 }  // namespace
@@ -813,6 +835,8 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   check(cake_model_launch_count(g.model, &launches0, 1), "launch count");
 
   // ---------------------------------------------------------------- t = 0
+  NvtxScope nv_run(std::string("bidirectional run: ") + (mode == RunMode::cake ? "cake" : mode == RunMode::io_only ? "io_only" : "compute_only") +
+                   ", " + std::to_string(n) + " chunks");
   RunTimer timer;
   LiveRun run(g, plan, timer);
   run.tp = tp;
@@ -926,6 +950,7 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
                                                     backend.last_launched() == static_cast<int>(n - 1));
   const long long T = static_cast<long long>(tail.token_start + tail.token_count);
   if (tp) tp->publish_final(tail_hidden ? 0 : 1, static_cast<int>(tail.token_count) - 1);
+  NvtxScope nv_final(std::string("first token") + (tail_hidden ? "" : " (recompute last token)"));
   check(cake_event_record(g.ev_final_start->h, g.s_compute), "record");
   check(cake_final_logits(g.model, T, g.tokens.p + (T - 1), tail_hidden ? 0 : 1, static_cast<int>(tail.token_count) - 1,
                           g.final_bt, g.logits.p, g.s_compute),
