@@ -33,7 +33,7 @@ def workload_config(T, C, mbps, world):
     return {"workload": f"llama3-8b-shape T={T} chunk={C} tier=pinned-DRAM link={mbps}mbps "
                         f"({mbps / 8000:g} GB/s) bidirectional+race", "model": "llama-3-8b-shape", "seq_len": T,
             "chunk": C, "link_mbps": mbps,
-            "parallelism": f"tp{world} (KV-head sharded, NCCL all-reduce)" if world > 1 else "1 GPU",
+            "parallelism": f"tp{world} (KV-head sharded, peer-memory reductions)" if world > 1 else "1 GPU",
             "l2": "inputs larger than L2 (16 GB weights, 4 GiB KV tier) — no flush"}
 
 
@@ -267,29 +267,42 @@ def b200_arm(args):
 
         from paper_2410_03065_b200 import native as N
 
+        if args.share_device:  # functional check of the multi-process path on one GPU
+            local = 0
         torch.cuda.set_device(local)
-        td.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if args.share_device:
+            td.init_process_group("gloo")
+        else:
+            td.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         dist = td
-        # ONE request, KV-head-sharded over the group. NCCL id and
-        # coordinator name from rank 0; the model's own communicator carries the
-        # two per-layer all-reduces (torch's only does barriers / the max below).
+        # ONE request, KV-head-sharded over the group; coordinator
+        # name from rank 0. The per-layer reductions run over peer memory
+        # (tp_peer.cuh, CUDA IPC handles all-gathered below) or, with
+        # --tp-reduce nccl, the baseline ncclAllReduce on the model's own
+        # communicator (torch's group only does barriers / the max below).
         cl = N.load_cuda()
         uid = (ctypes.c_uint8 * 128)()
-        if rank == 0 and cl.cake_nccl_unique_id(uid) != 0:
+        if args.tp_reduce == "nccl" and rank == 0 and cl.cake_nccl_unique_id(uid) != 0:
             raise RuntimeError("ncclGetUniqueId failed")
         obj = [bytes(uid), f"/cake_tp_{uuid.uuid4().hex[:16]}"]
         td.broadcast_object_list(obj, src=0)
-        ctypes.memmove(uid, obj[0], 128)
-        comm = ctypes.c_void_p()
-        cl.cake_cuda_set_device(local)
-        if cl.cake_nccl_init(ctypes.byref(comm), uid, world, rank) != 0:
-            raise RuntimeError("ncclCommInitRank failed")
-        tp_kw = dict(tp_rank=rank, tp_size=world, nccl_comm=comm.value, tp_shm=obj[1])
+        tp_kw = dict(tp_rank=rank, tp_size=world, tp_shm=obj[1])
+        if args.tp_reduce == "nccl":
+            ctypes.memmove(uid, obj[0], 128)
+            comm = ctypes.c_void_p()
+            cl.cake_cuda_set_device(local)
+            if cl.cake_nccl_init(ctypes.byref(comm), uid, world, rank) != 0:
+                raise RuntimeError("ncclCommInitRank failed")
+            tp_kw["nccl_comm"] = comm.value
     from paper_2410_03065_b200.runtime import GpuRuntime
 
     T, C, mbps = args.tokens, args.chunk, args.mbps
     seed = 42  # every TP rank serves the same prompt
     rt = GpuRuntime("llama3_8b", max_tokens=T, max_chunk=C, device=local, **tp_kw)
+    if world > 1 and args.tp_reduce == "peer":
+        handles = [None] * world
+        dist.all_gather_object(handles, rt.tp_peer_handles())
+        rt.tp_peer_open(handles)
     rt.calibrate(T, C, seed)
     tier = rt.build_cache_tier(T, C, seed)
 
@@ -444,6 +457,10 @@ def main():
     ap.add_argument("--no-race", action="store_true")
     ap.add_argument("--no-profile", dest="profile", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tp-reduce", default="peer", choices=["peer", "nccl"],
+                    help="TP reductions: one peer-memory kernel (product) or ncclAllReduce (baseline)")
+    ap.add_argument("--share-device", action="store_true",
+                    help="every rank on GPU 0 (functional check of the multi-process path on one GPU)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: launch our own ranks when not started by torchrun

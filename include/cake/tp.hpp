@@ -11,7 +11,12 @@
 //                     its own KV-head shard of them (its own emulated link);
 //   shard landed      per-chunk counters: a chunk is io-committed only when
 //                     every rank's shard is in HBM;
-//   final step        recompute flag / tail row of the first-token step.
+//   final step        recompute flag / tail row of the first-token step, and
+//                     whether the contested chunk's pages are the spare set;
+//   race-to-finish    the racer's entry carries kRaceBit (followers write that
+//                     chunk through their own spare page set); every commit is
+//                     published (decided), so followers abort the losing
+//                     side's work on the contested chunk the same way.
 // State lives in a POSIX shared-memory segment of lock-free atomics.
 #pragma once
 
@@ -44,6 +49,9 @@ class TpCoordinator {
   void end_run();
 
   // Leader publishes, followers consume entry k (blocking; nullopt = sequence ended).
+  // Entries are chunk indices, or'ed with kRaceBit for the racer's entry of the
+  // contested chunk.
+  static constexpr std::uint32_t kRaceBit = 1u << 30;
   void publish_compute(std::uint32_t chunk);
   void end_compute();
   std::optional<std::uint32_t> next_compute(std::uint32_t k);
@@ -51,12 +59,22 @@ class TpCoordinator {
   void end_io();
   std::optional<std::uint32_t> next_io(std::uint32_t k);
 
-  // Every rank reports its shard of `chunk` landed; the leader waits for all.
+  // Every rank reports its shard of `chunk` landed; the leader waits for all
+  // (false: the compute side committed the chunk first, the loads were dropped).
   void shard_landed(std::uint32_t chunk);
-  void wait_all_landed(std::uint32_t chunk);
+  bool wait_all_landed(std::uint32_t chunk);
 
-  void publish_final(int recompute, int last_row);
-  std::pair<int, int> wait_final();
+  // Commit decisions (side 1 = compute, 2 = io); 0 = undecided.
+  void publish_decided(std::uint32_t chunk, int side);
+  int decided(std::uint32_t chunk) const;
+  struct Final {
+    int recompute = 0, last_row = 0;
+    int race_pages = -1;  // contested chunk whose winner wrote the spare page set, or -1
+    int race_chunk = -1, race_winner = -1;  // the run's contest (0 compute, 1 io won), for the report
+  };
+  void publish_final(const Final& f);
+  Final wait_final();
+  bool final_published() const;
 
  private:
   struct Shared;

@@ -234,8 +234,15 @@ CAKE_API int cake_tp_end_io(cake_tp* t);
 CAKE_API int cake_tp_next_io(cake_tp* t, uint32_t k, uint32_t* chunk, int* has);
 CAKE_API int cake_tp_shard_landed(cake_tp* t, uint32_t chunk);
 CAKE_API int cake_tp_wait_all_landed(cake_tp* t, uint32_t chunk);
-CAKE_API int cake_tp_publish_final(cake_tp* t, int recompute, int last_row);
-CAKE_API int cake_tp_wait_final(cake_tp* t, int* recompute, int* last_row);
+/* Entries of the compute / io sequences are chunk indices; the racer's entry of
+ * the contested chunk carries CAKE_TP_RACE_BIT (race-to-finish mirrored). */
+#define CAKE_TP_RACE_BIT (1u << 30)
+/* Commit decisions: side 1 = compute, 2 = io (0 = undecided). */
+CAKE_API int cake_tp_publish_decided(cake_tp* t, uint32_t chunk, int side);
+CAKE_API int cake_tp_decided(cake_tp* t, uint32_t chunk, int* side);
+/* race_pages: the contested chunk whose winner wrote the spare page set, or -1. */
+CAKE_API int cake_tp_publish_final(cake_tp* t, int recompute, int last_row, int race_pages);
+CAKE_API int cake_tp_wait_final(cake_tp* t, int* recompute, int* last_row, int* race_pages);
 
 #ifdef __cplusplus
 }

@@ -142,8 +142,21 @@ CAKE_API int cake_nccl_destroy(void* comm);
  * the all-reduce. Verifies the sharding on a single GPU. */
 CAKE_API int cake_prefill_group(cake_model** models, int n, const int32_t* d_tokens, long long chunk_start,
                                 int chunk_len, const int32_t* d_block_table, void* stream);
-/* Attach an NCCL communicator (ncclComm_t) for tp_size > 1. */
+/* Attach an NCCL communicator (ncclComm_t) for tp_size > 1 (the baseline
+ * reduction: fp32 ncclAllReduce + add + rmsnorm kernels). */
 CAKE_API int cake_model_set_comm(cake_model* m, void* nccl_comm);
+/* Peer-memory TP (the product reduction, csrc/cuda/tp_peer.cuh): after each
+ * row-parallel projection ONE kernel pulls the peers' bf16 partials of this
+ * rank's row slice over NVLink, adds them in rank order into the residual,
+ * applies the next RMSNorm and pushes the normalized rows into every rank's
+ * activation buffer. Replaces the two ncclAllReduce calls per layer of the
+ * north-star design (reference wiring: proj/src/scheduler.cpp:229-278 runs
+ * one compute agent; here one per GPU in lockstep).
+ * Every rank exports CAKE_TP_PEER_HANDLE_BYTES of CUDA IPC handles; the
+ * launcher all-gathers them (rank order) and every rank opens the set. */
+#define CAKE_TP_PEER_HANDLE_BYTES 256
+CAKE_API int cake_tp_peer_handles(cake_model* m, void* out, size_t cap);
+CAKE_API int cake_tp_peer_open(cake_model* m, const void* all_handles, int nranks);
 
 enum {
   CAKE_PREFILL_NO_KV_WRITE = 1 /* q-only pass (first-token step over a complete cache) */

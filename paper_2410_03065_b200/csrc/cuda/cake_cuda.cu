@@ -25,6 +25,7 @@
 #endif
 #include "cake_cuda.h"
 #include "elementwise.cuh"
+#include "tp_peer.cuh"
 #include "gemm.cuh"
 #include "gemm2.cuh"
 #include "gemm2c.cuh"
@@ -587,6 +588,14 @@ struct cake_model {
   int attn_impl = 0;        // 0 product dispatch, 1 mma.sync (cross-check), 2 one-tile / 3 two-tile tcgen05 only
   int* attn_tickets = nullptr;  // split arrival tickets of the two-tile kernel (zero at rest)
   ncclComm_t comm = nullptr;
+  // peer-memory TP (tp_peer.cuh): IPC mappings of every rank's exchange buffers
+  bool peer_tp = false;
+  unsigned long long* tp_flags = nullptr;  // own flag block (kTpFlagWords)
+  void* peer_part[kTpMaxRanks]{};
+  bf16* peer_xn[kTpMaxRanks]{};
+  float* peer_h[kTpMaxRanks]{};
+  unsigned long long* peer_flags[kTpMaxRanks]{};
+  unsigned long long tp_epoch = 0;
   bool emulated_tp = false;  // test driver sums the ranks' partials itself (cake_prefill_group)
   unsigned profile_mask = 0;  // bit k: bracket launches of kernel class k with events
   int profile_stride = 1;     // bracket every n-th launch of a class (keeps the other PDL chains intact)
@@ -925,6 +934,37 @@ int launch_skinny(cake_model* m, int kind, const SkinnyArgs& a, double rows, cud
   return CAKE_OK;
 }
 
+// Peer-memory TP reduction of this rank's partial in tp_buf (tp_peer.cuh):
+// slice mode (M > 1): h row slices += rank-ordered sum, RMSNorm(gamma) rows
+// pushed into every rank's xn; replicated (M = 1): every rank's full h.
+int tp_reduce(cake_model* m, int M, bool replicated, const bf16* gamma, cudaStream_t s) {
+  TpReduceArgs a{};
+  const int n = m->cfg.tp_size;
+  for (int r = 0; r < n; ++r) {
+    a.part[r] = m->peer_part[r];
+    a.xn[r] = m->peer_xn[r];
+    a.flags[r] = m->peer_flags[r];
+  }
+  a.h = m->h;
+  a.gamma = gamma;
+  a.eps = m->cfg.rms_eps;
+  a.rank = m->cfg.tp_rank;
+  a.nranks = n;
+  a.M = M;
+  a.H = m->H;
+  a.replicated = replicated ? 1 : 0;
+  a.epoch = ++m->tp_epoch;
+  const int rows = replicated ? M : (M + n - 1) / n;
+  const int grid = std::max(1, std::min(rows, num_sms()));
+  // wire bytes of this rank: pulled partials of its rows (+ pushed normalized rows)
+  const double elt = replicated ? 4.0 : 2.0;
+  const double bytes = static_cast<double>(rows) * m->H * (elt * n + (replicated ? 0.0 : 2.0 * n) + 8.0);
+  ProfScope ps(m, CAKE_K_ALLREDUCE, s, 0.0, bytes);
+  tp_reduce_kernel<<<grid, kTpThreads, 0, s>>>(a);
+  CKL();
+  return CAKE_OK;
+}
+
 // Row-parallel skinny projection into the residual stream (TP: partials + all-reduce).
 int skinny_row_parallel(cake_model* m, int kind, const bf16* W, const bf16* x, int K, cudaStream_t s) {
   SkinnyArgs a{};
@@ -938,10 +978,11 @@ int skinny_row_parallel(cake_model* m, int kind, const bf16* W, const bf16* x, i
     a.ldr = m->H;
     return launch_skinny<kSkResid>(m, kind, a, m->H, s);
   }
-  if (!m->comm) return fail(CAKE_ESTATE, "tp_size > 1 but no NCCL communicator attached");
+  if (!m->comm && !m->peer_tp) return fail(CAKE_ESTATE, "tp_size > 1 but no peer mappings / NCCL communicator");
   a.out = m->tp_buf;
   a.ldo = m->H;
   CKS(launch_skinny<kSkF32>(m, kind, a, m->H, s));
+  if (m->peer_tp) return tp_reduce(m, 1, true, nullptr, s);
   {
     ProfScope ps(m, CAKE_K_ALLREDUCE, s, 0.0, 4.0 * m->H);
     ncclResult_t r = ncclAllReduce(m->tp_buf, m->tp_buf, static_cast<size_t>(m->H), ncclFloat32, ncclSum, m->comm, s);
@@ -1115,7 +1156,7 @@ int rmsnorm(cake_model* m, const bf16* gamma, long long row0, int rows, const in
 
 // Row-parallel projection output: residual += acc (TP: via all-reduce of partials).
 int row_parallel(cake_model* m, int kind, const CUtensorMap* ta, const CUtensorMap* tb, int K, int M,
-                 const int32_t* abort_flag, cudaStream_t s) {
+                 const int32_t* abort_flag, cudaStream_t s, const bf16* next_gamma) {
   GemmArgs g{};
   g.M = M;
   g.N = m->H;
@@ -1134,9 +1175,18 @@ int row_parallel(cake_model* m, int kind, const CUtensorMap* ta, const CUtensorM
     ProfScope ps(m, kind, s, flops, bytes);
     return gemm_dispatch(128, kEpiResid, ta, tb, g, s, g.xb_out != nullptr ? m->out_h : nullptr);
   }
-  if (!m->comm && !m->emulated_tp) return fail(CAKE_ESTATE, "tp_size > 1 but no NCCL communicator attached");
+  if (!m->comm && !m->emulated_tp && !m->peer_tp)
+    return fail(CAKE_ESTATE, "tp_size > 1 but no peer mappings / NCCL communicator");
   g.out = m->tp_buf;
   g.ldo = m->H;
+  if (m->peer_tp) {
+    // bf16 partial (half the wire bytes of fp32), then the fused reduce + RMSNorm + push
+    {
+      ProfScope ps(m, kind, s, flops, bytes);
+      CKS(gemm_dispatch(128, kEpiBf16, ta, tb, g, s));
+    }
+    return tp_reduce(m, M, false, next_gamma, s);
+  }
   {
     ProfScope ps(m, kind, s, flops, bytes);
     CKS(gemm_dispatch(128, kEpiF32, ta, tb, g, s));
@@ -1162,8 +1212,10 @@ int layer_attention_half(cake_model* m, int l, long long chunk_start, int M, con
                          const int32_t* d_abort, bool no_kv, cudaStream_t s) {
   const int H = m->H;
   LayerWeights& lw = m->layers[l];
-  const bool fused = fused_norm(m) && l > 0;  // layer 0's input is the embedding (no producer epilogue)
-  if (!fused) CKS(rmsnorm(m, lw.ln1, 0, M, d_abort, s));
+  // layer 0's input is the embedding (no producer epilogue); peer TP: the down
+  // reduction of layer l-1 already wrote norm(h) rows into xn
+  const bool fused = fused_norm(m) && l > 0;
+  if (!fused && !(m->peer_tp && l > 0)) CKS(rmsnorm(m, lw.ln1, 0, M, d_abort, s));
   {
     GemmArgs g{};
     if (fused) set_norm_consumer(m, g);
@@ -1189,14 +1241,14 @@ int layer_attention_half(cake_model* m, int l, long long chunk_start, int M, con
     CKS(gemm_dispatch(t192 ? 192 : m->bn_qkv, kEpiQkv, m->a_xn, t192 ? lw.m_qkv192 : lw.m_qkv, g, s));
   }
   CKS(attention(m, chunk_start, M, l, d_block_table, d_abort, s));
-  return row_parallel(m, CAKE_K_GEMM_O, m->a_attn, lw.m_o, m->nq * m->hd, M, d_abort, s);
+  return row_parallel(m, CAKE_K_GEMM_O, m->a_attn, lw.m_o, m->nq * m->hd, M, d_abort, s, lw.ln2);
 }
 
 int layer_mlp_half(cake_model* m, int l, int M, const int32_t* d_abort, cudaStream_t s) {
   const int H = m->H;
   LayerWeights& lw = m->layers[l];
   const bool fused = fused_norm(m);
-  if (!fused) CKS(rmsnorm(m, lw.ln2, 0, M, d_abort, s));
+  if (!fused && !m->peer_tp) CKS(rmsnorm(m, lw.ln2, 0, M, d_abort, s));  // peer TP: the O reduction wrote xn
   {
     GemmArgs g{};
     if (fused) set_norm_consumer(m, g);
@@ -1209,7 +1261,8 @@ int layer_mlp_half(cake_model* m, int l, int M, const int32_t* d_abort, cudaStre
     ProfScope ps(m, CAKE_K_GEMM_GU, s, 2.0 * M * g.N * H, 2.0 * g.N * H + 2.0 * M * H + 2.0 * M * m->F);
     CKS(gemm_dispatch(256, kEpiSwiglu, m->a_xn, lw.m_gu, g, s));
   }
-  return row_parallel(m, CAKE_K_GEMM_D, m->a_act, lw.m_d, m->F, M, d_abort, s);
+  return row_parallel(m, CAKE_K_GEMM_D, m->a_act, lw.m_d, m->F, M, d_abort, s,
+                      l + 1 < m->L ? m->layers[l + 1].ln1 : m->final_norm);
 }
 
 }  // namespace
@@ -1405,9 +1458,16 @@ int cake_model_destroy(cake_model* m) {
                   static_cast<void*>(m->q), static_cast<void*>(m->attn), static_cast<void*>(m->act),
                   static_cast<void*>(m->part_o), static_cast<void*>(m->part_lse),
                   static_cast<void*>(m->tp_buf), static_cast<void*>(m->q8_ws), static_cast<void*>(m->ss),
-                  static_cast<void*>(m->dec_bar),
+                  static_cast<void*>(m->dec_bar), static_cast<void*>(m->tp_flags),
                   static_cast<void*>(m->attn_tickets)})
     if (p) cudaFree(p);
+  if (m->peer_tp)
+    for (int r = 0; r < m->cfg.tp_size; ++r)
+      if (r != m->cfg.tp_rank) {
+        for (void* p : {m->peer_part[r], static_cast<void*>(m->peer_xn[r]), static_cast<void*>(m->peer_h[r]),
+                        static_cast<void*>(m->peer_flags[r])})
+          if (p) cudaIpcCloseMemHandle(p);
+      }
   for (auto& p : m->prof) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
@@ -1587,6 +1647,12 @@ int cake_model_create_shared(const cake_model_config* cfg, const cake_model* par
   cudaMemset(m->attn_tickets, 0, R * m->nkv * sizeof(int));
   if (c.tp_size > 1 && (st = alloc_dev(reinterpret_cast<void**>(&m->tp_buf), R * H * sizeof(float))))
     return bail(st);
+  if (c.tp_size > 1) {
+    if (c.tp_size > kTpMaxRanks) return bail(fail(CAKE_EINVAL, "model: tp_size > %d", kTpMaxRanks));
+    if ((st = alloc_dev(reinterpret_cast<void**>(&m->tp_flags), kTpFlagWords * sizeof(unsigned long long))))
+      return bail(st);
+    cudaMemset(m->tp_flags, 0, kTpFlagWords * sizeof(unsigned long long));
+  }
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->q8_ws), 2 * sizeof(unsigned)))) return bail(st);
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->dec_bar), 2 * sizeof(unsigned)))) return bail(st);
   cudaMemset(m->dec_bar, 0, 2 * sizeof(unsigned));
@@ -1669,6 +1735,48 @@ int cake_model_set_attention_impl(cake_model* m, int impl) {
     return fail(CAKE_EINVAL, "attention impl must be 0 (product dispatch), 1 (mma.sync), 2 (one-tile tcgen05), "
                              "3 (two-tile tcgen05) or 4 (one-tile, decoupled softmax groups)");
   m->attn_impl = impl;
+  return CAKE_OK;
+}
+
+int cake_tp_peer_handles(cake_model* m, void* out, size_t cap) {
+  if (!m || !out) return fail(CAKE_EINVAL, "tp peer: null");
+  if (m->cfg.tp_size < 2) return fail(CAKE_ESTATE, "tp peer: model is not tensor-parallel");
+  if (cap < CAKE_TP_PEER_HANDLE_BYTES) return fail(CAKE_EINVAL, "tp peer: need %d bytes", CAKE_TP_PEER_HANDLE_BYTES);
+  static_assert(4 * sizeof(cudaIpcMemHandle_t) <= CAKE_TP_PEER_HANDLE_BYTES, "handle blob");
+  auto* h = static_cast<cudaIpcMemHandle_t*>(out);
+  void* bufs[4] = {m->tp_buf, m->xn, m->h, m->tp_flags};
+  for (int i = 0; i < 4; ++i) CK(cudaIpcGetMemHandle(&h[i], bufs[i]));
+  return CAKE_OK;
+}
+
+int cake_tp_peer_open(cake_model* m, const void* all, int nranks) {
+  if (!m || !all) return fail(CAKE_EINVAL, "tp peer: null");
+  if (nranks != m->cfg.tp_size) return fail(CAKE_EINVAL, "tp peer: %d handle sets for tp_size %d", nranks, m->cfg.tp_size);
+  if (m->peer_tp) return fail(CAKE_ESTATE, "tp peer: already open");
+  const auto* blob = static_cast<const unsigned char*>(all);
+  for (int r = 0; r < nranks; ++r) {
+    if (r == m->cfg.tp_rank) {
+      m->peer_part[r] = m->tp_buf;
+      m->peer_xn[r] = m->xn;
+      m->peer_h[r] = m->h;
+      m->peer_flags[r] = m->tp_flags;
+      continue;
+    }
+    const auto* h = reinterpret_cast<const cudaIpcMemHandle_t*>(blob + static_cast<size_t>(r) * CAKE_TP_PEER_HANDLE_BYTES);
+    void* p[4] = {};
+    for (int i = 0; i < 4; ++i) {
+      cudaError_t e = cudaIpcOpenMemHandle(&p[i], h[i], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        for (int j = 0; j < i; ++j) cudaIpcCloseMemHandle(p[j]);
+        return fail(CAKE_ECUDA + e, "tp peer: open rank %d buffer %d: %s", r, i, cudaGetErrorString(e));
+      }
+    }
+    m->peer_part[r] = p[0];
+    m->peer_xn[r] = static_cast<bf16*>(p[1]);
+    m->peer_h[r] = static_cast<float*>(p[2]);
+    m->peer_flags[r] = static_cast<unsigned long long*>(p[3]);
+  }
+  m->peer_tp = true;
   return CAKE_OK;
 }
 
@@ -1799,6 +1907,14 @@ int cake_final_logits(cake_model* m, long long T, const int32_t* d_last_token, i
     row = 0;
   }
   if (row < 0 || row >= m->rows_cap) return fail(CAKE_EINVAL, "final: bad row");
+  if (m->peer_tp && !recompute) {
+    // prefill left h sharded by rows (row r on rank r % N): fetch the tail row
+    // from its owner (final since this rank's last reduction saw every peer's B flag)
+    const int owner = row % m->cfg.tp_size;
+    if (owner != m->cfg.tp_rank)
+      CK(cudaMemcpyAsync(m->h + static_cast<size_t>(row) * m->H, m->peer_h[owner] + static_cast<size_t>(row) * m->H,
+                         m->H * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  }
   {
     ProfScope ps(m, CAKE_K_RMSNORM, s, 0.0, m->H * 6.0);
     rmsnorm_kernel<<<1, kNormThreadsPerRow * kNormRowsPerCta, 0, s>>>(m->h, m->final_norm, m->xn, m->H,

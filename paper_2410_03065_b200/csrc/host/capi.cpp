@@ -615,12 +615,21 @@ int cake_tp_next_io(cake_tp* t, uint32_t k, uint32_t* chunk, int* has) {
   });
 }
 int cake_tp_shard_landed(cake_tp* t, uint32_t chunk) { return guarded([&] { t->c->shard_landed(chunk); }); }
-int cake_tp_wait_all_landed(cake_tp* t, uint32_t chunk) { return guarded([&] { t->c->wait_all_landed(chunk); }); }
-int cake_tp_publish_final(cake_tp* t, int recompute, int last_row) {
-  return guarded([&] { t->c->publish_final(recompute, last_row); });
+int cake_tp_wait_all_landed(cake_tp* t, uint32_t chunk) { return guarded([&] { (void)t->c->wait_all_landed(chunk); }); }
+int cake_tp_publish_decided(cake_tp* t, uint32_t chunk, int side) {
+  return guarded([&] { t->c->publish_decided(chunk, side); });
 }
-int cake_tp_wait_final(cake_tp* t, int* recompute, int* last_row) {
-  return guarded([&] { std::tie(*recompute, *last_row) = t->c->wait_final(); });
+int cake_tp_decided(cake_tp* t, uint32_t chunk, int* side) { return guarded([&] { *side = t->c->decided(chunk); }); }
+int cake_tp_publish_final(cake_tp* t, int recompute, int last_row, int race_pages) {
+  return guarded([&] { t->c->publish_final({recompute, last_row, race_pages}); });
+}
+int cake_tp_wait_final(cake_tp* t, int* recompute, int* last_row, int* race_pages) {
+  return guarded([&] {
+    const auto f = t->c->wait_final();
+    *recompute = f.recompute;
+    *last_row = f.last_row;
+    *race_pages = f.race_pages;
+  });
 }
 #endif  // CAKE_REFERENCE_BUILD
 

@@ -161,6 +161,7 @@ struct GpuContext::Impl {
   Device<std::int32_t> bt_primary, bt_race, tokens, abort_flags;
   Pinned<std::int32_t> h_bt_race, h_tokens, h_abort_one;
   Device<std::byte> staging[2];
+  Pinned<std::byte> follower_landing;  // TP follower, file tier: one chunk (reused; each chunk's copies are synced)
   std::size_t staging_bytes = 0;
   Device<float> logits;
   Pinned<float> h_logits;
@@ -303,6 +304,16 @@ void upload_tokens(GpuContext::Impl& g, const std::vector<std::uint32_t>& ids, v
     g.h_tokens.p[i] = static_cast<std::int32_t>(ids[i]);
   }
   check(cake_h2d_async(g.tokens.p, g.h_tokens.p, ids.size() * sizeof(std::int32_t), stream), "tokens H2D");
+}
+
+// Second page set for a contested chunk: the chunk's logical pages map to
+// the spare physical pages, every other page to itself. Uploaded on the
+// racer's stream ahead of the racer's writes.
+void upload_race_table(GpuContext::Impl& g, const ChunkSpec& c, void* stream) {
+  const int first = static_cast<int>(c.token_start / g.cfg.page_tokens);
+  for (int p = 0; p < g.n_pages; ++p) g.h_bt_race.p[p] = p;
+  for (int p = 0; p < g.pages_of(c); ++p) g.h_bt_race.p[first + p] = g.n_pages + p;
+  check(cake_h2d_async(g.bt_race.p, g.h_bt_race.p, g.n_pages * sizeof(std::int32_t), stream), "race bt");
 }
 
 }  // namespace
@@ -476,6 +487,7 @@ struct LiveRun {
     }
     int expected = kNone;
     if (!commit[i].compare_exchange_strong(expected, who)) return false;
+    if (tp) tp->publish_decided(i, who == kByCompute ? 1 : 2);  // followers drop the loser's work too
     nvtx_mark("commit chunk " + std::to_string(i) + (who == kByCompute ? " by compute" : " by io"));
     {
       std::lock_guard lk(commit_mu);
@@ -511,10 +523,7 @@ struct LiveRun {
   void start_race(const ChunkSpec& c, int who, void* stream) {
     if (race_chunk.load() != static_cast<int>(c.index) || racer.load() != who)
       throw std::logic_error("race: chunk contested without the race slot");
-    const int first = static_cast<int>(c.token_start / g.cfg.page_tokens);
-    for (int p = 0; p < g.n_pages; ++p) g.h_bt_race.p[p] = p;
-    for (int p = 0; p < g.pages_of(c); ++p) g.h_bt_race.p[first + p] = g.n_pages + p;
-    check(cake_h2d_async(g.bt_race.p, g.h_bt_race.p, g.n_pages * sizeof(std::int32_t), stream), "race bt");
+    upload_race_table(g, c, stream);
   }
 
   // Which page table each side writes a chunk through.
@@ -540,7 +549,8 @@ class GpuPrefillBackend final : public PrefillBackend {
   void launch(const ChunkSpec& c, bool contested) override {
     GpuContext::Impl& g = r_.g;
     NvtxScope nv("compute chunk " + std::to_string(c.index) + (contested ? " (contested)" : ""));
-    if (r_.tp) r_.tp->publish_compute(c.index);  // followers enqueue the same chunk (NCCL lockstep)
+    // followers enqueue the same chunk (reduction lockstep), the racer's entry through their spare pages
+    if (r_.tp) r_.tp->publish_compute(c.index | (contested ? TpCoordinator::kRaceBit : 0u));
     const Micros predicted = predict_finish(c);
     if (contested) r_.start_race(c, kByCompute, g.s_compute);
     const std::int32_t* bt = r_.table_for(c.index, kByCompute);
@@ -638,7 +648,8 @@ class GpuLoaderSink final : public ChunkSink {
     GpuContext::Impl& g = r_.g;
     if (range_) nvtxRangeEnd(range_);  // an abandoned chunk never reached end_chunk
     range_ = nvtxRangeStartA(("load chunk " + std::to_string(t.chunk.index) + (t.contested ? " (contested)" : "")).c_str());
-    if (r_.tp) r_.tp->publish_io(t.chunk.index);  // every rank loads its shard of this chunk
+    // every rank loads its shard of this chunk (the racer's entry into its spare pages)
+    if (r_.tp) r_.tp->publish_io(t.chunk.index | (t.contested ? TpCoordinator::kRaceBit : 0u));
     if (t.contested) r_.start_race(t.chunk, kByIo, g.s_copy);
     // quant8: land the 4-B header at +12 so the level payload is 16-B aligned
     buf_ = g.staging[parity_].p + (q8_ ? kQ8Offset : 0);
@@ -670,7 +681,7 @@ class GpuLoaderSink final : public ChunkSink {
     check(cake_event_sync(r_.g.ev_io[t.chunk.index]->h), "io wait");
     if (r_.tp) {  // resident only when every rank's KV-head shard landed
       r_.tp->shard_landed(t.chunk.index);
-      r_.tp->wait_all_landed(t.chunk.index);
+      if (!r_.tp->wait_all_landed(t.chunk.index)) return -1;  // compute landed it first
     }
     if (!r_.try_commit(t.chunk.index, kByIo)) return -1;  // compute landed it first
     r_.abort_compute(t.chunk.index);  // stop any compute work still queued for it
@@ -711,6 +722,8 @@ RunReport run_follower(GpuContext::Impl& g, TpCoordinator& tp, const RunPlan& pl
   const Micros t0 = timer.now_us();
   check(cake_stream_wait_event(g.s_copy, g.ev_anchor->h), "order");
   check(cake_memset_async(g.abort_flags.p, 0, g.n_pages * sizeof(std::int32_t), g.s_compute), "abort reset");
+  check(cake_event_record(g.ev_reset->h, g.s_compute), "record");  // abort writes (s_control) after the reset
+  check(cake_stream_wait_event(g.s_control, g.ev_reset->h), "order");
   upload_tokens(g, tokens, g.s_compute);
   auto dev_time = [&](void* ev) {
     float ms = 0.f;
@@ -726,21 +739,31 @@ RunReport run_follower(GpuContext::Impl& g, TpCoordinator& tp, const RunPlan& pl
       for (std::uint32_t k = 0;; ++k) {
         const auto c = tp.next_io(k);
         if (!c) break;
-        const std::uint32_t i = *c;
+        const std::uint32_t i = *c & ~TpCoordinator::kRaceBit;
+        const bool racer = (*c & TpCoordinator::kRaceBit) != 0;
+        if (racer) upload_race_table(g, plan.chunks[i], g.s_copy);
+        const std::int32_t* bt = racer ? g.bt_race.p : g.bt_primary.p;
         const std::uint64_t total = plan.encoded_bytes[i];
         ChunkReader rd = store.open_reader(plan.keys[i]);
-        std::vector<std::byte> host;  // file tier: read whole chunk (memory tier: zero-copy view)
+        // file tier: read the whole chunk into pinned memory (the slice H2Ds below are
+        // async); memory tier: zero-copy view of the pinned tier
         const std::byte* src = nullptr;
         if (rd.in_memory()) {
           src = rd.view_next(static_cast<std::size_t>(total)).data();
         } else {
-          host.resize(static_cast<std::size_t>(total));
+          if (g.follower_landing.n < total) g.follower_landing.reset(static_cast<std::size_t>(total));
+          std::span<std::byte> host(g.follower_landing.p, static_cast<std::size_t>(total));
           if (rd.read(host) != host.size()) throw CorruptChunkError("tp follower: short read");
           src = host.data();
         }
         const bool q8 = plan.encoded_bytes[i] != plan.uncompressed_bytes[i];
         std::byte* buf = g.staging[k & 1].p + (q8 ? 12 : 0);
+        bool abandoned = false;
         for (std::uint64_t off = 0; off < total;) {
+          if (tp.decided(i) == 1) {  // the leader's compute side committed this chunk: drop the load
+            abandoned = true;
+            break;
+          }
           const std::uint64_t len = std::min(quantum, total - off);
           const Micros gate = budget + time_to_transfer_bits(trace, len * 8, budget);
           timer.sleep_until_us_precise(gate);
@@ -751,13 +774,14 @@ RunReport run_follower(GpuContext::Impl& g, TpCoordinator& tp, const RunPlan& pl
           const Micros one = time_to_transfer_bits(trace, quantum * 8, budget);
           if (budget + one < now) budget = now - one;
         }
+        if (abandoned) continue;
         if (q8)
           check(cake_kv_scatter_q8(g.model, buf, static_cast<long long>(plan.chunks[i].token_start),
-                                   static_cast<int>(plan.chunks[i].token_count), g.bt_primary.p, g.s_copy),
+                                   static_cast<int>(plan.chunks[i].token_count), bt, g.s_copy),
                 "q8 decode-scatter");
         else
           check(cake_kv_scatter(g.model, buf, static_cast<long long>(plan.chunks[i].token_start),
-                                static_cast<int>(plan.chunks[i].token_count), g.bt_primary.p, 0,
+                                static_cast<int>(plan.chunks[i].token_count), bt, 0,
                                 static_cast<long long>(total), g.s_copy),
                 "scatter");
         check(cake_event_record(g.ev_io[i]->h, g.s_copy), "record");
@@ -773,34 +797,75 @@ RunReport run_follower(GpuContext::Impl& g, TpCoordinator& tp, const RunPlan& pl
   for (std::uint32_t k = 0;; ++k) {
     const auto c = tp.next_compute(k);
     if (!c) break;
-    const ChunkSpec& ch = plan.chunks[*c];
+    const ChunkSpec& ch = plan.chunks[*c & ~TpCoordinator::kRaceBit];
+    const bool racer = (*c & TpCoordinator::kRaceBit) != 0;
+    if (racer) upload_race_table(g, ch, g.s_compute);
     check(cake_event_record(g.ev_start[ch.index]->h, g.s_compute), "record");
     check(cake_prefill_chunk(g.model, g.tokens.p + ch.token_start, static_cast<long long>(ch.token_start),
-                             static_cast<int>(ch.token_count), g.bt_primary.p, nullptr, 0, g.s_compute),
+                             static_cast<int>(ch.token_count), racer ? g.bt_race.p : g.bt_primary.p,
+                             g.abort_flags.p + ch.index, 0, g.s_compute),
           "prefill");
     check(cake_event_record(g.ev_end[ch.index]->h, g.s_compute), "record");
     computed.push_back(ch.index);
   }
-  const auto [recompute, last_row] = tp.wait_final();
+  // the leader's loader won a chunk this rank is computing (the contested one,
+  // either racer): cancel its queued kernels like the leader does (the
+  // reductions still run, so the ranks stay in lockstep)
+  std::vector<char> aborted(n, 0);
+  auto maybe_abort = [&] {
+    for (std::uint32_t i : computed)
+      if (!aborted[i] && tp.decided(i) == 2) {
+        check(cake_h2d_async(g.abort_flags.p + i, g.h_abort_one.p, sizeof(std::int32_t), g.s_control), "abort");
+        aborted[i] = 1;
+      }
+  };
+  while (!tp.final_published()) {
+    maybe_abort();
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  maybe_abort();
+  const TpCoordinator::Final fin = tp.wait_final();
+  const int recompute = fin.recompute, last_row = fin.last_row;
+  g.final_bt = fin.race_pages >= 0 ? g.bt_race.p : g.bt_primary.p;
   io.join();
   if (io_error) std::rethrow_exception(io_error);
   const ChunkSpec& tail = plan.chunks[n - 1];
   const long long T = static_cast<long long>(tail.token_start + tail.token_count);
-  check(cake_final_logits(g.model, T, g.tokens.p + (T - 1), recompute, last_row, g.bt_primary.p, g.logits.p,
+  check(cake_event_record(g.ev_final_start->h, g.s_compute), "record");
+  check(cake_final_logits(g.model, T, g.tokens.p + (T - 1), recompute, last_row, g.final_bt, g.logits.p,
                           g.s_compute),
         "final logits");
-  check(cake_stream_sync(g.s_compute), "sync");
+  check(cake_d2h_async(g.h_logits.p, g.logits.p, g.cfg.vocab * sizeof(float), g.s_compute), "logits D2H");
+  check(cake_event_record(g.ev_logits->h, g.s_compute), "record");
+  check(cake_event_sync(g.ev_logits->h), "logits");
+  GpuRunInfo info;
+  info.first_token_us = timer.now_us();
   RunReport rep;
   rep.mode = mode;
   rep.n_chunks = n;
+  // the leader's commits decide which side delivered each chunk (a contested one ran on both)
   for (std::uint32_t i : computed)
-    rep.chunks.push_back({i, Side::compute, dev_time(g.ev_start[i]->h), dev_time(g.ev_end[i]->h), 0});
+    if (tp.decided(i) != 2)
+      rep.chunks.push_back({i, Side::compute, dev_time(g.ev_start[i]->h), dev_time(g.ev_end[i]->h), 0});
   for (std::uint32_t i : io_chunks)
-    rep.chunks.push_back({i, Side::io, 0, dev_time(g.ev_io[i]->h), plan.encoded_bytes[i]});
+    if (tp.decided(i) != 1) rep.chunks.push_back({i, Side::io, 0, dev_time(g.ev_io[i]->h), plan.encoded_bytes[i]});
   detail::finalize_report(rep, 0);
   rep.merge_point = detail::merge_from_records(rep);
   rep.computed_fraction = static_cast<double>(rep.merge_point) / n;
-  g.final_bt = g.bt_primary.p;
+  float ms = 0.f;
+  check(cake_event_elapsed_ms(g.ev_final_start->h, g.ev_logits->h, &ms), "elapsed");
+  info.final_step_us = static_cast<Micros>(std::llround(ms * 1000.0));
+  check(cake_event_elapsed_ms(g.ev_anchor->h, g.ev_logits->h, &ms), "elapsed");
+  info.device_ttft_ms = ms;
+  info.kv_resident_us = rep.ttft_us;
+  info.merge_point = rep.merge_point;
+  info.raced_chunk = fin.race_chunk;
+  info.race_winner = fin.race_winner;
+  info.recomputed_last = recompute != 0;
+  info.d2h_bytes = g.cfg.vocab * sizeof(float);
+  check(cake_model_launch_count(g.model, &info.kernel_launches, 0), "launch count");
+  info.logits.assign(g.h_logits.p, g.h_logits.p + g.cfg.vocab);
+  g.last = std::move(info);
   tp.end_run();
   return rep;
 }
@@ -827,7 +892,7 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   TpCoordinator* tp = g.tp.get();
   if (tp && !plan.suffix.empty()) throw std::invalid_argument("gpu run: partially cached prompts are single-GPU only");
   if (tp && !tp->leader()) return run_follower(g, *tp, plan, tokens, trace, store, mode, opt);
-  const bool race = opt.race_to_finish && io_on && compute_on && tp == nullptr;  // TP: boundary race not mirrored yet
+  const bool race = opt.race_to_finish && io_on && compute_on;  // TP: mirrored through the coordinator
   g.ensure_events(n_all);
   if (tp) tp->begin_run(++g.run_counter, n);
   sync_own_streams(g);
@@ -881,6 +946,13 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
     tasks.reserve(n);
     for (std::uint32_t i = n; i-- > 0;) tasks.push_back({plan.keys[i], plan.chunks[i], plan.encoded_bytes[i]});
     loader->push_seq(std::move(tasks));
+    if (race && opt.race_force == 1) {
+      // test hook: the compute side starts once the loader is pacing its first chunk, so
+      // there is an in-flight chunk to contest however the host threads get scheduled
+      const Micros deadline = timer.now_us() + 10'000'000;
+      while (!loader->inflight_finish_estimate(n - 1) && timer.now_us() < deadline)
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
   }
 
   RunReport rep;
@@ -949,7 +1021,9 @@ RunReport run_live_gpu(const RunPlan& plan, const std::vector<std::uint32_t>& to
   const bool tail_hidden = !plan.suffix.empty() || (run.commit[n - 1].load() == kByCompute &&
                                                     backend.last_launched() == static_cast<int>(n - 1));
   const long long T = static_cast<long long>(tail.token_start + tail.token_count);
-  if (tp) tp->publish_final(tail_hidden ? 0 : 1, static_cast<int>(tail.token_count) - 1);
+  if (tp)
+    tp->publish_final({tail_hidden ? 0 : 1, static_cast<int>(tail.token_count) - 1, racer_won ? rc : -1, rc,
+                       rc >= 0 ? (run.commit[rc].load() == kByCompute ? 0 : 1) : -1});
   NvtxScope nv_final(std::string("first token") + (tail_hidden ? "" : " (recompute last token)"));
   check(cake_event_record(g.ev_final_start->h, g.s_compute), "record");
   check(cake_final_logits(g.model, T, g.tokens.p + (T - 1), tail_hidden ? 0 : 1, static_cast<int>(tail.token_count) - 1,

@@ -21,10 +21,11 @@ struct TpCoordinator::Shared {
   std::atomic<std::int32_t> compute_count, compute_end;
   std::atomic<std::int32_t> io_count, io_end;
   std::atomic<std::int32_t> final_set;
-  std::atomic<std::int32_t> final_recompute, final_last_row;
+  std::atomic<std::int32_t> final_recompute, final_last_row, final_race_pages, final_race_chunk, final_race_winner;
   std::atomic<std::int32_t> compute_seq[kMaxChunks];
   std::atomic<std::int32_t> io_seq[kMaxChunks];
   std::atomic<std::int32_t> landed[kMaxChunks];
+  std::atomic<std::int32_t> decided[kMaxChunks];
 };
 
 namespace {
@@ -89,7 +90,10 @@ void TpCoordinator::begin_run(std::uint64_t run_id, std::uint32_t n_chunks) {
     sh_->io_count.store(0);
     sh_->io_end.store(0);
     sh_->final_set.store(0);
-    for (std::uint32_t i = 0; i < n_chunks; ++i) sh_->landed[i].store(0, std::memory_order_relaxed);
+    for (std::uint32_t i = 0; i < n_chunks; ++i) {
+      sh_->landed[i].store(0, std::memory_order_relaxed);
+      sh_->decided[i].store(0, std::memory_order_relaxed);
+    }
     sh_->n_chunks.store(n_chunks);
     sh_->run_id.store(run_id, std::memory_order_release);
     spin_until([&] { return sh_->followers_ready.load(std::memory_order_acquire) >= size_ - 1; });
@@ -147,19 +151,36 @@ std::optional<std::uint32_t> TpCoordinator::next_io(std::uint32_t k) {
 
 void TpCoordinator::shard_landed(std::uint32_t chunk) { sh_->landed[chunk].fetch_add(1, std::memory_order_acq_rel); }
 
-void TpCoordinator::wait_all_landed(std::uint32_t chunk) {
-  spin_until([&] { return sh_->landed[chunk].load(std::memory_order_acquire) >= size_; });
+bool TpCoordinator::wait_all_landed(std::uint32_t chunk) {
+  bool all = false;
+  spin_until([&] {
+    all = sh_->landed[chunk].load(std::memory_order_acquire) >= size_;
+    return all || sh_->decided[chunk].load(std::memory_order_acquire) == 1;
+  });
+  return all;
 }
 
-void TpCoordinator::publish_final(int recompute, int last_row) {
-  sh_->final_recompute.store(recompute, std::memory_order_relaxed);
-  sh_->final_last_row.store(last_row, std::memory_order_relaxed);
+void TpCoordinator::publish_decided(std::uint32_t chunk, int side) {
+  sh_->decided[chunk].store(side, std::memory_order_release);
+}
+
+int TpCoordinator::decided(std::uint32_t chunk) const { return sh_->decided[chunk].load(std::memory_order_acquire); }
+
+void TpCoordinator::publish_final(const Final& f) {
+  sh_->final_recompute.store(f.recompute, std::memory_order_relaxed);
+  sh_->final_last_row.store(f.last_row, std::memory_order_relaxed);
+  sh_->final_race_pages.store(f.race_pages, std::memory_order_relaxed);
+  sh_->final_race_chunk.store(f.race_chunk, std::memory_order_relaxed);
+  sh_->final_race_winner.store(f.race_winner, std::memory_order_relaxed);
   sh_->final_set.store(1, std::memory_order_release);
 }
 
-std::pair<int, int> TpCoordinator::wait_final() {
+bool TpCoordinator::final_published() const { return sh_->final_set.load(std::memory_order_acquire) != 0; }
+
+TpCoordinator::Final TpCoordinator::wait_final() {
   spin_until([&] { return sh_->final_set.load(std::memory_order_acquire) != 0; });
-  return {sh_->final_recompute.load(), sh_->final_last_row.load()};
+  return {sh_->final_recompute.load(), sh_->final_last_row.load(), sh_->final_race_pages.load(),
+          sh_->final_race_chunk.load(), sh_->final_race_winner.load()};
 }
 
 }  // namespace cake

@@ -130,8 +130,10 @@ _SIGS = {
     "cake_tp_next_io": (C.c_int, [vp, u32, P(u32), P(C.c_int)]),
     "cake_tp_shard_landed": (C.c_int, [vp, u32]),
     "cake_tp_wait_all_landed": (C.c_int, [vp, u32]),
-    "cake_tp_publish_final": (C.c_int, [vp, C.c_int, C.c_int]),
-    "cake_tp_wait_final": (C.c_int, [vp, P(C.c_int), P(C.c_int)]),
+    "cake_tp_publish_decided": (C.c_int, [vp, u32, C.c_int]),
+    "cake_tp_decided": (C.c_int, [vp, u32, P(C.c_int)]),
+    "cake_tp_publish_final": (C.c_int, [vp, C.c_int, C.c_int, C.c_int]),
+    "cake_tp_wait_final": (C.c_int, [vp, P(C.c_int), P(C.c_int), P(C.c_int)]),
 }
 
 
@@ -219,7 +221,12 @@ def load_cuda():
     lib.cake_final_logits.argtypes = [vp, C.c_longlong, vp, C.c_int, C.c_int, vp, vp, vp]
     lib.cake_nccl_unique_id.argtypes = [vp]
     lib.cake_nccl_init.argtypes = [C.POINTER(vp), vp, C.c_int, C.c_int]
+    lib.cake_tp_peer_handles.argtypes = [vp, vp, C.c_size_t]
+    lib.cake_tp_peer_open.argtypes = [vp, vp, C.c_int]
     return lib
+
+
+TP_PEER_HANDLE_BYTES = 256  # include/cake_cuda.h CAKE_TP_PEER_HANDLE_BYTES
 
 
 def make_trace(points):

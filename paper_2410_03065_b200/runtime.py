@@ -18,6 +18,12 @@ import numpy as np
 from . import native as N
 from .cake import MODES, BandwidthTrace, ChunkStore, _opts, _records
 
+
+def _cuda_error(cu) -> str:
+    buf = C.create_string_buffer(512)
+    cu.cake_cuda_last_error(buf, len(buf))
+    return buf.value.decode(errors="replace")
+
 PRESETS = {
     # name: (n_layers, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab)
     "llama3_8b": (32, 4096, 32, 8, 128, 14336, 128256),
@@ -104,6 +110,24 @@ class GpuRuntime:
         self.max_chunk = max_chunk
         self._parent = weights_from  # shared weights: the parent context must outlive this one
         self._link = None
+
+    def tp_peer_handles(self) -> bytes:
+        """This rank's CUDA IPC handles of its TP exchange buffers (peer-memory reduction)."""
+        cu = N.load_cuda()
+        buf = (C.c_uint8 * N.TP_PEER_HANDLE_BYTES)()
+        if cu.cake_tp_peer_handles(self.n.lib.cake_gpu_model(self.h), buf, len(buf)) != 0:
+            raise RuntimeError(f"cake_tp_peer_handles: {_cuda_error(cu)}")
+        return bytes(buf)
+
+    def tp_peer_open(self, handles: list) -> None:
+        """Map every rank's exchange buffers (handles in rank order, this rank's included)."""
+        cu = N.load_cuda()
+        blob = b"".join(handles)
+        if len(blob) != N.TP_PEER_HANDLE_BYTES * len(handles):
+            raise ValueError("tp_peer_open: bad handle blobs")
+        buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        if cu.cake_tp_peer_open(self.n.lib.cake_gpu_model(self.h), buf, len(handles)) != 0:
+            raise RuntimeError(f"cake_tp_peer_open: {_cuda_error(cu)}")
 
     def close(self):
         if getattr(self, "h", None):

@@ -1,0 +1,134 @@
+"""Head-sharded TP as it runs on a multi-GPU box — one process per rank, the
+leader/follower coordinator (cake/tp.hpp), peer-memory reductions
+(csrc/cuda/tp_peer.cuh) over CUDA IPC mappings — with both ranks on one
+B200 (the processes' contexts time-slice the device, so every flag wait
+really waits on the other process).
+
+Each rank builds its KV-head shard of the cache tier and serves the same
+request in compute-only, I/O-only and bidirectional mode (the reference wiring
+of proj/src/scheduler.cpp:229-278, mirrored across ranks). Checked against the
+unsharded model on the same device:
+  * every rank's computed KV shard == the unsharded model's heads (2^-7 RMS),
+  * first-token logits: same top-1, RMS error <= 2^-7 (bf16 partials on the wire),
+  * loaded KV (I/O-only run) bit-exact vs the rank's own tier shard,
+  * bidirectional logits bit-identical to the rank's compute-only logits.
+"""
+import os
+import uuid
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+DIMS = (2, 1024, 8, 4, 128, 2048, 32000)  # GQA 2:1, 2 KV heads per rank at TP=2
+T, CH, SEED = 1024, 256, 45
+TOL = 2.0 ** -7
+
+
+# tests/test_gpu_parity.py's forced races (RunOptions::race_force / race_hold), on the TP group:
+# the leader decides, the follower writes the contested chunk through its own spare pages
+RACES = {
+    # a slower link than the single-GPU test: two processes time-slice the device, so compute is slower
+    "compute_racer_wins": dict(race_force=1, race_hold=1, mbps=20, racer="compute", winner=0),
+    "compute_racer_loses": dict(race_force=1, race_hold=0, mbps=20, racer="compute", winner=1),
+    "io_racer_wins": dict(race_force=2, race_hold=0, mbps=1_000_000, racer="io", winner=1),
+    "io_racer_loses": dict(race_force=2, race_hold=1, mbps=1_000_000, racer="io", winner=0),
+}
+
+
+def rms_rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.sqrt(np.mean((a - b) ** 2)) / np.sqrt(np.mean(b ** 2)))
+
+
+def _rank(rank, world, port, shm, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2410_03065_b200.runtime import GpuRuntime
+
+        rt = GpuRuntime(DIMS, max_tokens=T, max_chunk=CH, tp_rank=rank, tp_size=world, tp_shm=shm, device=0)
+        handles = [None] * world
+        dist.all_gather_object(handles, rt.tp_peer_handles())
+        rt.tp_peer_open(handles)
+        tier = rt.build_cache_tier(T, CH, SEED)
+        out = {"rank": rank}
+        runs = {"compute_only": dict(mode="compute_only", mbps=2000), "io_only": dict(mode="io_only", mbps=2000),
+                "cake": dict(mode="cake", mbps=2000)}
+        for case, spec in RACES.items():  # forced boundary races, mirrored on the follower
+            quantum = (1 << 20) if spec["racer"] == "compute" else rt.kv_bytes_per_token * CH
+            runs[case] = dict(mode="cake", mbps=spec["mbps"], quantum=quantum, race_force=spec["race_force"],
+                              race_hold=spec["race_hold"])
+        for name, kw in runs.items():
+            rt.poison(0xFF)
+            r = rt.run(tier, T, CH, SEED, **kw)
+            out[name] = {"logits": rt.logits().copy(), "merge": r.merge_point, "raced": r.raced_chunk,
+                         "winner": r.race_winner, "recomputed": r.recomputed_last,
+                         "kv": [rt.read_chunk(s, CH) for s in range(0, T, CH)]}
+        q.put(out)
+        dist.barrier()
+        rt.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tp2_peer_two_processes_one_gpu():
+    import torch
+    import torch.multiprocessing as mp
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2410_03065_b200.runtime import GpuRuntime
+
+    full = GpuRuntime(DIMS, max_tokens=T, max_chunk=CH)
+    tier = full.build_cache_tier(T, CH, SEED)
+    full.run(tier, T, CH, SEED, mbps=2000, mode="compute_only")
+    want_logits = full.logits().copy()
+    want_kv = [np.frombuffer(full.read_chunk(s, CH), np.uint16) for s in range(0, T, CH)]
+    full.close()
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + (os.getpid() % 2000)
+    shm = f"/cake_tp_peer_{uuid.uuid4().hex[:12]}"
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, shm, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted((q.get(timeout=600) for _ in procs), key=lambda o: o["rank"])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+
+    import llama_oracle
+
+    L, H, nh, nkv, hd, ffn, V = DIMS
+    half = nkv // 2
+    for o in outs:
+        r = o["rank"]
+        c = o["compute_only"]
+        for k, s in enumerate(range(0, T, CH)):
+            ref = llama_oracle.bf16_to_f32(want_kv[k]).reshape(L, 2, nkv, CH, hd)[:, :, r * half:(r + 1) * half]
+            got = llama_oracle.bf16_to_f32(np.frombuffer(c["kv"][k], np.uint16)).reshape(L, 2, half, CH, hd)
+            assert np.isfinite(got).all()
+            assert rms_rel(got, ref) <= TOL, (r, s, rms_rel(got, ref))
+        for mode in ("compute_only", "io_only", "cake"):
+            lg = o[mode]["logits"]
+            assert np.isfinite(lg).all(), (r, mode)
+            assert rms_rel(lg, want_logits) <= TOL, (r, mode, rms_rel(lg, want_logits))
+            assert int(lg.argmax()) == int(want_logits.argmax()), (r, mode)
+        # loaded shards are the computed ones byte for byte (the tier was built by this rank's compute pass),
+        # whichever side delivered each chunk and whoever won the contested one
+        for name in ["io_only", "cake"] + list(RACES):
+            for k in range(T // CH):
+                assert o[name]["kv"][k] == c["kv"][k], (r, name, k)
+        for case, spec in RACES.items():
+            res = o[case]
+            assert res["raced"] >= 0 and res["winner"] == spec["winner"], (r, case, res["raced"], res["winner"])
+            want = o["io_only"]["logits"] if res["recomputed"] else c["logits"]
+            assert np.array_equal(res["logits"], want), (r, case)
+    # every rank ends with the same logits (replicated LM head over the same reduced rows)
+    for name in ["cake"] + list(RACES):
+        assert np.array_equal(outs[0][name]["logits"], outs[1][name]["logits"]), name

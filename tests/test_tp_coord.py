@@ -19,6 +19,9 @@ import torch.multiprocessing as mp
 from paper_2410_03065_b200 import native as N
 
 
+RACE_BIT = 1 << 30  # include/cake_c.h CAKE_TP_RACE_BIT
+
+
 def _split(n, run):
     # compute takes the prefix, io the suffix backward (the bidirectional shape);
     # the merge point moves between runs
@@ -38,7 +41,7 @@ def _worker(rank, world, port, shm, n, runs, q):
         for run in range(1, runs + 1):
             lib.call("cake_tp_begin_run", t, run, n)
             comp, io_seq = _split(n, run)
-            got_c, got_io, final = [], [], None
+            got_c, got_io, final, raced = [], [], None, []
             if rank == 0:
                 def loader():
                     for i in io_seq:
@@ -49,13 +52,15 @@ def _worker(rank, world, port, shm, n, runs, q):
                 th = threading.Thread(target=loader)
                 th.start()
                 for i in comp:
-                    lib.call("cake_tp_publish_compute", t, i)
+                    lib.call("cake_tp_publish_compute", t, i | (RACE_BIT if i == comp[-1] else 0))
                     got_c.append(i)
                 lib.call("cake_tp_end_compute", t)
                 th.join()
                 lib.call("cake_tp_end_io", t)
-                lib.call("cake_tp_publish_final", t, run % 2, 17 + run)
-                final = (run % 2, 17 + run)
+                # the contested chunk of this run: compute's last entry raced (kRaceBit), io won it
+                lib.call("cake_tp_publish_decided", t, comp[-1], 2)
+                lib.call("cake_tp_publish_final", t, run % 2, 17 + run, comp[-1])
+                final = (run % 2, 17 + run, comp[-1], 2)
             else:
                 def mirror_io():
                     k = 0
@@ -75,14 +80,19 @@ def _worker(rank, world, port, shm, n, runs, q):
                     lib.call("cake_tp_next_compute", t, k, C.byref(c), C.byref(has))
                     if not has.value:
                         break
-                    got_c.append(c.value)
+                    got_c.append(c.value & ~RACE_BIT)
+                    if c.value & RACE_BIT:
+                        raced.append(c.value & ~RACE_BIT)
                     k += 1
-                rc, row = C.c_int(), C.c_int()
-                lib.call("cake_tp_wait_final", t, C.byref(rc), C.byref(row))
-                final = (rc.value, row.value)
+                rc, row, race, side = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+                lib.call("cake_tp_wait_final", t, C.byref(rc), C.byref(row), C.byref(race))
+                lib.call("cake_tp_decided", t, race.value, C.byref(side))
+                final = (rc.value, row.value, race.value, side.value)
                 th.join()
             lib.call("cake_tp_end_run", t)
-            seen.append((got_c, got_io, final))
+            if rank == 0:
+                raced = [comp[-1]]
+            seen.append((got_c, got_io, final, raced))
         everyone = [None] * world
         dist.all_gather_object(everyone, seen)
         lib.call("cake_tp_destroy", t)
@@ -107,12 +117,13 @@ def test_tp_coordinator_world2(n):
         p.join(timeout=60)
         assert p.exitcode == 0
     leader, follower = everyone
-    for run, (lc, li, lf) in enumerate(leader, start=1):
-        fc, fi, ff = follower[run - 1]
+    for run, (lc, li, lf, lr) in enumerate(leader, start=1):
+        fc, fi, ff, fr = follower[run - 1]
+        assert fr == lr  # the racer's entry carried the race bit
         comp, io_seq = _split(n, run)
         assert lc == comp and fc == comp
         assert li == io_seq and fi == io_seq
-        assert lf == ff == (run % 2, 17 + run)
+        assert lf == ff == (run % 2, 17 + run, comp[-1], 2)
         assert sorted(comp + io_seq) == list(range(n))
 
 
