@@ -16,6 +16,8 @@ waves = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "1,2,4,7").split
 cl = N.load_cuda()
 rt = GpuRuntime("llama3_8b", max_tokens=T, max_chunk=512)
 tier = rt.build_cache_tier(T, 512, 42)
+if os.environ.get("IMPL"):
+    rt.set_attention_impl(os.environ["IMPL"])  # e.g. tcgen05_s3
 for rep in range(2):
     for w in waves:
         cl.cake_set_experiment(2, w)
