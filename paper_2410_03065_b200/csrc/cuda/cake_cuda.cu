@@ -581,7 +581,7 @@ struct cake_model {
   float* tp_buf = nullptr;  // fp32 partial sums for the TP all-reduce
   float* ss = nullptr;      // fused RMSNorm: [H / 128][rows_cap] partial sums of squares of the residual rows
   unsigned* q8_ws = nullptr;  // quant8 encode: ordered min/max keys
-  unsigned* dec_bar = nullptr;  // first-token chain kernel: grid barrier (arrivals, generation)
+  unsigned* dec_bar = nullptr;  // first-token chain kernel: grid barrier (one monotone 64-bit arrival counter)
   CUtensorMap a_xn[3], a_attn[3], a_act[3];
   CUtensorMap out_h[2];  // staged residual epilogue: h (fp32, 32-col boxes), xn = bf16(h) (64-col boxes)  // activation maps, boxes of 128 / 64 / 32 rows (gemm2c pieces)
   CUtensorMap tm_q, tm_kv;  // attention: Q rows of a GQA group, paged K/V pool
@@ -1000,7 +1000,9 @@ int rmsnorm(cake_model* m, const bf16* gamma, long long row0, int rows, const in
 // projection of `q_layer` (q_layer >= 0), one CTA per SM, grid barriers
 // between the phases. Cooperative launch: every CTA is resident before any
 // spins in a barrier (two contexts' chains never split the SMs between them).
-int g_dec_prefetch_kb = 128;  // L2 prefetch per CTA ahead of each chain phase (A/B: cake_dec_set_prefetch)
+int g_dec_prefetch_kb = 64;  // L2 prefetch per CTA ahead of each chain phase (A/B: cake_dec_set_prefetch; 0/32/64/128 KB: 3.79/3.71/3.68/3.69 ms)
+long long* g_dec_trace = nullptr;  // debug: cake_dec_debug_trace
+int g_dec_trace_layer = -2;
 int dec_chain(cake_model* m, int layer, int q_layer, long long pos, cudaStream_t s) {
   DecArgs a{};
   auto add = [&](int kind, const bf16* W, const bf16* gamma, int K, int units) {
@@ -1032,7 +1034,8 @@ int dec_chain(cake_model* m, int layer, int q_layer, long long pos, cudaStream_t
   a.rope = m->rope;
   a.pos = pos;
   a.head_dim = m->hd;
-  a.gbar = m->dec_bar;
+  a.gbar = reinterpret_cast<unsigned long long*>(m->dec_bar);
+  if (g_dec_trace != nullptr && g_dec_trace_layer == layer) a.trace = g_dec_trace;
   const size_t smem = static_cast<size_t>(a.max_k) * 2 + sizeof(float) * a.red_rows;
   static bool cfgd = false;
   if (!cfgd) {
@@ -2039,6 +2042,14 @@ int cake_dec_set_prefetch(int kb) {
 int cake_set_experiment(int knob, int value) {
   if (knob < 0 || knob >= CAKE_EXP_COUNT) return fail(CAKE_EINVAL, "experiment knob %d out of range", knob);
   g_exp[knob] = value;
+  return CAKE_OK;
+}
+
+// Debug: %globaltimer stamps of every CTA of the decode chain launch for `layer`
+// ([cta][16]: entry, after the PDL wait, then per phase: start, x staged, rows done).
+CAKE_API int cake_dec_debug_trace(long long* dev_buf, int layer) {
+  g_dec_trace = dev_buf;
+  g_dec_trace_layer = dev_buf != nullptr ? layer : -2;
   return CAKE_OK;
 }
 

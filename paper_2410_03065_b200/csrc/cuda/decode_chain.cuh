@@ -62,8 +62,17 @@ struct DecArgs {
   const float2* rope;         // [pos][hd / 2]
   long long pos;
   int head_dim;
-  unsigned* gbar;             // grid barrier: [0] arrivals, [1] generation
+  unsigned long long* gbar;   // grid barrier: monotone arrival counter
+  long long* trace;           // debug (cake_dec_debug_trace): %globaltimer per CTA [cta][16]
 };
+
+__device__ __forceinline__ void dec_stamp(const DecArgs& a, int slot) {
+  if (a.trace != nullptr && threadIdx.x == 0) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[blockIdx.x * 16 + slot] = t;
+  }
+}
 
 __device__ __forceinline__ int dec_rows_per_unit(int kind) { return (kind == kDecQ || kind == kDecGU) ? 2 : 1; }
 
@@ -99,17 +108,18 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) 
                : "memory");
 }
 
-// Ask L2 for the first `budget` bytes of this CTA's rows of phase p (one thread).
-__device__ __forceinline__ void dec_prefetch(const DecArgs& a, int p, int cta, int ctas) {
+// Ask L2 for the first `budget` bytes of this CTA's rows of phase p; lane l
+// of the calling warp issues rows l, l+32, ... (one bulk prefetch per row),
+// so the issue takes one round instead of a serial loop.
+__device__ __forceinline__ void dec_prefetch(const DecArgs& a, int p, int cta, int ctas, int lane) {
   if (p >= a.n_phases) return;
   const DecPhase ph = dec_phase(a, p);
   const int rpu = dec_rows_per_unit(ph.kind);
   int u0, u1;
   dec_range(ph.units, cta, ctas, u0, u1);
   const uint32_t row_bytes = static_cast<uint32_t>(ph.K) * 2u;
-  int budget = a.prefetch_bytes;
-  for (int ri = u0 * rpu; ri < u1 * rpu && budget > 0; ++ri, budget -= static_cast<int>(row_bytes))
-    prefetch_l2_bulk(dec_row(ph, ri, a.head_dim), row_bytes);
+  const int n = min((u1 - u0) * rpu, static_cast<int>((static_cast<uint32_t>(a.prefetch_bytes) + row_bytes - 1) / row_bytes));
+  for (int i = lane; i < n; i += 32) prefetch_l2_bulk(dec_row(ph, u0 * rpu + i, a.head_dim), row_bytes);
 }
 
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
@@ -118,21 +128,35 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
   return v;
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // All CTAs of the grid (one per SM, all resident: cooperative launch) meet
-// here; the phase's global writes are visible to every CTA after it.
-__device__ __forceinline__ void dec_grid_barrier(unsigned* gbar, int ctas) {
+// here; the phase's global writes are visible to every CTA after it. One
+// monotone 64-bit arrival counter (never reset): barrier k completes when it
+// reaches (k+1) * ctas, which each CTA derives from its own atomicAdd — one
+// L2 round trip for the last arrival instead of reset + generation bump.
+// `between` runs after this CTA arrived and before it waits (the L2 prefetch
+// of the next phase's rows), so it costs no barrier time.
+template <typename F>
+__device__ __forceinline__ void dec_grid_barrier(unsigned long long* ctr, int ctas, F&& between) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned gen = ld_acquire_gpu(gbar + 1);
-    __threadfence();
-    if (atomicAdd(gbar, 1u) == static_cast<unsigned>(ctas) - 1u) {
-      atomicExch(gbar, 0u);
+  if (threadIdx.x < 32) {  // warp 0: lane 0 arrives, then the warp issues the prefetches, then lane 0 waits
+    unsigned long long target = 0;
+    if (threadIdx.x == 0) {
       __threadfence();
-      atomicAdd(gbar + 1, 1u);
-    } else {
-      while (ld_acquire_gpu(gbar + 1) == gen) __nanosleep(20);
+      const unsigned long long old = atomicAdd(ctr, 1ull);
+      target = (old / static_cast<unsigned long long>(ctas) + 1ull) * ctas;
     }
-    __threadfence();
+    __syncwarp();
+    between(static_cast<int>(threadIdx.x));
+    if (threadIdx.x == 0) {
+      while (ld_acquire_gpu_u64(ctr) < target) __nanosleep(32);  // (a tight spin floods the counter's L2 line)
+      __threadfence();
+    }
   }
   __syncthreads();
 }
@@ -159,16 +183,16 @@ __global__ void __launch_bounds__(kDecThreads, 1) dec_chain_kernel(const DecArgs
   const int ctas = gridDim.x;
   const int cta = blockIdx.x;
 
-  if (tid == 0) dec_prefetch(a, 0, cta, ctas);  // weights do not depend on the predecessor
+  dec_stamp(a, 0);
+  if (tid < 32) dec_prefetch(a, 0, cta, ctas, tid);  // weights do not depend on the predecessor
   pdl_wait();  // the first phase's input (attn / h) is the predecessor's output
   pdl_trigger();
+  dec_stamp(a, 1);
 #pragma unroll 1
   for (int p = 0; p < a.n_phases; ++p) {
     const DecPhase ph = dec_phase(a, p);
-    if (p > 0) {
-      if (tid == 0) dec_prefetch(a, p, cta, ctas);
-      dec_grid_barrier(a.gbar, ctas);
-    }
+    if (p > 0) dec_grid_barrier(a.gbar, ctas, [&](int ln) { dec_prefetch(a, p, cta, ctas, ln); });
+    dec_stamp(a, 2 + 3 * p);
     const int K = ph.K;
     // ---- x of the phase into shared memory (bf16)
     if (ph.kind == kDecQ || ph.kind == kDecGU) {
@@ -203,6 +227,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) dec_chain_kernel(const DecArgs
       for (int c = tid; c < (K >> 3); c += kDecThreads) reinterpret_cast<uint4*>(xs)[c] = x[c];
     }
     __syncthreads();
+    dec_stamp(a, 3 + 3 * p);
     // ---- this CTA's rows, one warp per row at a time
     const int rpu = dec_rows_per_unit(ph.kind);
     int u0, u1;
@@ -232,6 +257,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) dec_chain_kernel(const DecArgs
       if (lane == 0) rsum[i] = s;
     }
     __syncthreads();
+    dec_stamp(a, 4 + 3 * p);
     // ---- epilogue: one thread per unit
     for (int i = tid; i < u1 - u0; i += kDecThreads) {
       const int uu = u0 + i;
