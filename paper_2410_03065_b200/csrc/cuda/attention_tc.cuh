@@ -63,6 +63,8 @@ struct FaArgs {
   float scale_log2;
   const int* abort_flag;
   long long* trace;  // debug (nullptr): clock64 stamps of CTA (0,0,0), tools/attn_trace.py
+  int stable_pages;  // logical pages [0, stable_pages) are not written by the predecessor kernel: their
+                     // K/V blocks are requested before the PDL wait (0: none)
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -164,6 +166,41 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  // The first ring's worth of K/V blocks over stable pages (the prefix before this chunk,
+  // or the whole cache for the q-only first-token pass) does not depend on the predecessor:
+  // requested before the PDL wait, so the ring fills under the predecessor's tail.
+  __shared__ int s_npre;
+  if (warp == 0 && lane == 0) {
+    int n_pre = 0;
+    if (tok0 < a.chunk_len) {
+      const long long planes0 = static_cast<long long>(a.n_layers) * 2 * a.n_kv_heads;
+      for (int j = 0; j < nb && j < Cfg::kKStages && j < Cfg::kVStages; ++j) {
+        const int lp0 = p_begin + 2 * j;
+        const int lp1 = (lp0 + 1 < p_end) ? lp0 + 1 : lp0;
+        if (lp1 >= a.stable_pages) break;
+        int32_t r[2][2];
+        for (int kv = 0; kv < 2; ++kv)
+          for (int q = 0; q < 2; ++q) {
+            const long long ph = a.block_table[q ? lp1 : lp0];
+            r[kv][q] = static_cast<int32_t>(
+                ((ph * planes0) + (static_cast<long long>(a.layer) * 2 + kv) * a.n_kv_heads + kvh) * 64);
+          }
+        mbar_arrive_expect_tx(&k_full[j], Cfg::kTileBytes);
+        mbar_arrive_expect_tx(&v_full[j], Cfg::kTileBytes);
+#pragma unroll
+        for (int h = 0; h < Cfg::kHalves; ++h) {
+          tma_load_2d(sK + j * Cfg::kTileBytes + h * Cfg::kHalfBytes, &tm_kv, &k_full[j], h * 64, r[0][0]);
+          tma_load_2d(sK + j * Cfg::kTileBytes + h * Cfg::kHalfBytes + Cfg::kPageHalfBytes, &tm_kv, &k_full[j],
+                      h * 64, r[0][1]);
+          tma_load_2d(sV + j * Cfg::kTileBytes + h * Cfg::kHalfBytes, &tm_kv, &v_full[j], h * 64, r[1][0]);
+          tma_load_2d(sV + j * Cfg::kTileBytes + h * Cfg::kHalfBytes + Cfg::kPageHalfBytes, &tm_kv, &v_full[j],
+                      h * 64, r[1][1]);
+        }
+        ++n_pre;
+      }
+    }
+    s_npre = n_pre;
+  }
   // (PDL) everything above overlaps the predecessor's tail; Q / the KV pool are read below
   pdl_wait();
   pdl_trigger();
@@ -172,7 +209,13 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int n_pre = s_npre;
   if (s_abort || tok0 >= a.chunk_len) {
+    if (warp == 0 && lane == 0)  // requested blocks must land before the shared memory goes away
+      for (int j = 0; j < n_pre; ++j) {
+        mbar_wait(&k_full[j], 0);
+        mbar_wait(&v_full[j], 0);
+      }
     if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tmem);
     return;
   }
@@ -185,7 +228,7 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
   if (warp == 0) {
     if (lane == 0 && nb > 0) {
       // ------------------------------------------------ TMA producer: K blocks
-      for (int j = 0; j < nb; ++j) {
+      for (int j = n_pre; j < nb; ++j) {
         const int s = j % Cfg::kKStages;
         mbar_wait(&k_empty[s], ((j / Cfg::kKStages) & 1) ^ 1u);
         const int lp0 = p_begin + 2 * j;
@@ -203,7 +246,7 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
   } else if (warp == 2) {
     if (lane == 0 && nb > 0) {
       // ------------------------------------------------ TMA producer: V blocks
-      for (int j = 0; j < nb; ++j) {
+      for (int j = n_pre; j < nb; ++j) {
         const int s = j % Cfg::kVStages;
         mbar_wait(&v_empty[s], ((j / Cfg::kVStages) & 1) ^ 1u);
         const int lp0 = p_begin + 2 * j;

@@ -824,6 +824,9 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
     fa.scale_log2 = 1.4426950408889634f / std::sqrt(static_cast<float>(m->hd));
     fa.abort_flag = abort_flag;
     fa.trace = (g_fa4_trace_layer == layer) ? g_fa4_trace : nullptr;
+    // pages the predecessor cannot be writing: the prefix before a (page-aligned) prefill chunk,
+    // or every page for the q-only first-token pass (unaligned start, no KV write)
+    fa.stable_pages = (chunk_start % kAttnPage) ? n_pages : static_cast<int>(chunk_start / kAttnPage);
 #ifdef CAKE_ATTN_VARIANTS
     if (m->attn_impl == 4) {  // decoupled softmax groups (attention_dec.cuh)
       if (m->hd == 128) {
