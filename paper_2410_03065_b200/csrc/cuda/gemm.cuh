@@ -190,7 +190,13 @@ struct StreamK {
 template <int BLOCK_N, int EPI>
 struct EpiPre {
   static constexpr bool kH = (EPI == kEpiResid) && BLOCK_N <= 128;
+  // QKV: the row's RoPE (cos, sin) pairs for both rope units of a head (hd 128: j = 0, 1;
+  // hd 64: j = 0) and the physical page of its position — loaded while the mainloop runs, so
+  // the epilogue after the accumulator is ready does no dependent global loads
+  static constexpr bool kQ = EPI == kEpiQkv;
   float4 h[kH ? BLOCK_N / 4 : 1];
+  float4 cs[kQ ? 2 : 1][kQ ? 16 : 1];
+  long long phys = 0;
   float rs = 1.f;
   __device__ __forceinline__ void load(const GemmArgs& a, int m, int n_blk, bool partial) {
     if (partial || m >= a.M) return;
@@ -203,6 +209,18 @@ struct EpiPre {
       const float4* src = reinterpret_cast<const float4*>(a.resid + static_cast<size_t>(m) * a.ldr + n_blk * BLOCK_N);
 #pragma unroll
       for (int q = 0; q < BLOCK_N / 4; ++q) h[q] = src[q];
+    }
+    if constexpr (kQ) {
+      const long long pos = a.pos0 + m;
+      const int half = a.head_dim >> 1;
+      const float4* c0 = reinterpret_cast<const float4*>(a.rope + pos * half);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) cs[0][i] = __ldg(c0 + i);
+      if (a.head_dim >= 128) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) cs[1][i] = __ldg(c0 + 16 + i);
+      }
+      if (a.n_kv_heads > 0) phys = a.block_table[pos / a.page_tokens];
     }
   }
 };
@@ -368,11 +386,10 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t tba
           if (!valid) continue;
           float o0[32], o1[32];
           if (region < 2) {
-            // (cos, sin) of dims i, i+1 in one 16-B load (rows of hd/2 float2 are 16-B aligned)
-            const float4* cs = reinterpret_cast<const float4*>(args.rope + pos * half + j * 32);
+            // (cos, sin) of dims i, i+1 (loaded with the epilogue inputs during the mainloop)
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
-              const float4 t = __ldg(cs + i / 2);
+              const float4 t = j == 0 ? pre.cs[0][i / 2] : pre.cs[1][i / 2];
               const float a0 = __uint_as_float(x0[i]), b0 = __uint_as_float(x1[i]);
               const float a1 = __uint_as_float(x0[i + 1]), b1 = __uint_as_float(x1[i + 1]);
               o0[i] = a0 * t.x - b0 * t.y;
@@ -394,7 +411,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t tba
             const int kvh = region == 1 ? head - args.n_q_heads : head - args.n_q_heads - args.n_kv_heads;
             const long long lpage = pos / args.page_tokens;
             const int slot = static_cast<int>(pos - lpage * args.page_tokens);
-            const long long phys = args.block_table[lpage];
+            const long long phys = pre.phys;
             const size_t off =
                 ((((static_cast<size_t>(phys) * args.n_layers + args.layer) * 2 + (region - 1)) *
                       args.n_kv_heads + kvh) * args.page_tokens + slot) * static_cast<size_t>(hd);
