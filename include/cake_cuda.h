@@ -152,9 +152,11 @@ CAKE_API int cake_model_set_comm(cake_model* m, void* nccl_comm);
  * activation buffer. Replaces the two ncclAllReduce calls per layer of the
  * north-star design (reference wiring: proj/src/scheduler.cpp:229-278 runs
  * one compute agent; here one per GPU in lockstep).
+ * The first-token LM head is vocab-sharded: each rank computes V/N logits and
+ * stores them into every rank's logits buffer.
  * Every rank exports CAKE_TP_PEER_HANDLE_BYTES of CUDA IPC handles; the
  * launcher all-gathers them (rank order) and every rank opens the set. */
-#define CAKE_TP_PEER_HANDLE_BYTES 256
+#define CAKE_TP_PEER_HANDLE_BYTES 512
 CAKE_API int cake_tp_peer_handles(cake_model* m, void* out, size_t cap);
 CAKE_API int cake_tp_peer_open(cake_model* m, const void* all_handles, int nranks);
 

@@ -594,6 +594,8 @@ struct cake_model {
   void* peer_part[kTpMaxRanks]{};
   bf16* peer_xn[kTpMaxRanks]{};
   float* peer_h[kTpMaxRanks]{};
+  float* tp_logits = nullptr;  // [vocab] first-token logits, assembled from every rank's vocab shard
+  float* peer_logits[kTpMaxRanks]{};
   unsigned long long* peer_flags[kTpMaxRanks]{};
   unsigned long long tp_epoch = 0;
   bool emulated_tp = false;  // test driver sums the ranks' partials itself (cake_prefill_group)
@@ -1464,14 +1466,14 @@ int cake_model_destroy(cake_model* m) {
                   static_cast<void*>(m->q), static_cast<void*>(m->attn), static_cast<void*>(m->act),
                   static_cast<void*>(m->part_o), static_cast<void*>(m->part_lse),
                   static_cast<void*>(m->tp_buf), static_cast<void*>(m->q8_ws), static_cast<void*>(m->ss),
-                  static_cast<void*>(m->dec_bar), static_cast<void*>(m->tp_flags),
+                  static_cast<void*>(m->dec_bar), static_cast<void*>(m->tp_flags), static_cast<void*>(m->tp_logits),
                   static_cast<void*>(m->attn_tickets)})
     if (p) cudaFree(p);
   if (m->peer_tp)
     for (int r = 0; r < m->cfg.tp_size; ++r)
       if (r != m->cfg.tp_rank) {
         for (void* p : {m->peer_part[r], static_cast<void*>(m->peer_xn[r]), static_cast<void*>(m->peer_h[r]),
-                        static_cast<void*>(m->peer_flags[r])})
+                        static_cast<void*>(m->peer_flags[r]), static_cast<void*>(m->peer_logits[r])})
           if (p) cudaIpcCloseMemHandle(p);
       }
   for (auto& p : m->prof) {
@@ -1657,6 +1659,8 @@ int cake_model_create_shared(const cake_model_config* cfg, const cake_model* par
     if (c.tp_size > kTpMaxRanks) return bail(fail(CAKE_EINVAL, "model: tp_size > %d", kTpMaxRanks));
     if ((st = alloc_dev(reinterpret_cast<void**>(&m->tp_flags), kTpFlagWords * sizeof(unsigned long long))))
       return bail(st);
+    if ((st = alloc_dev(reinterpret_cast<void**>(&m->tp_logits), static_cast<size_t>(c.vocab) * sizeof(float))))
+      return bail(st);
     cudaMemset(m->tp_flags, 0, kTpFlagWords * sizeof(unsigned long long));
   }
   if ((st = alloc_dev(reinterpret_cast<void**>(&m->q8_ws), 2 * sizeof(unsigned)))) return bail(st);
@@ -1748,10 +1752,10 @@ int cake_tp_peer_handles(cake_model* m, void* out, size_t cap) {
   if (!m || !out) return fail(CAKE_EINVAL, "tp peer: null");
   if (m->cfg.tp_size < 2) return fail(CAKE_ESTATE, "tp peer: model is not tensor-parallel");
   if (cap < CAKE_TP_PEER_HANDLE_BYTES) return fail(CAKE_EINVAL, "tp peer: need %d bytes", CAKE_TP_PEER_HANDLE_BYTES);
-  static_assert(4 * sizeof(cudaIpcMemHandle_t) <= CAKE_TP_PEER_HANDLE_BYTES, "handle blob");
+  static_assert(5 * sizeof(cudaIpcMemHandle_t) <= CAKE_TP_PEER_HANDLE_BYTES, "handle blob");
   auto* h = static_cast<cudaIpcMemHandle_t*>(out);
-  void* bufs[4] = {m->tp_buf, m->xn, m->h, m->tp_flags};
-  for (int i = 0; i < 4; ++i) CK(cudaIpcGetMemHandle(&h[i], bufs[i]));
+  void* bufs[5] = {m->tp_buf, m->xn, m->h, m->tp_flags, m->tp_logits};
+  for (int i = 0; i < 5; ++i) CK(cudaIpcGetMemHandle(&h[i], bufs[i]));
   return CAKE_OK;
 }
 
@@ -1766,11 +1770,12 @@ int cake_tp_peer_open(cake_model* m, const void* all, int nranks) {
       m->peer_xn[r] = m->xn;
       m->peer_h[r] = m->h;
       m->peer_flags[r] = m->tp_flags;
+      m->peer_logits[r] = m->tp_logits;
       continue;
     }
     const auto* h = reinterpret_cast<const cudaIpcMemHandle_t*>(blob + static_cast<size_t>(r) * CAKE_TP_PEER_HANDLE_BYTES);
-    void* p[4] = {};
-    for (int i = 0; i < 4; ++i) {
+    void* p[5] = {};
+    for (int i = 0; i < 5; ++i) {
       cudaError_t e = cudaIpcOpenMemHandle(&p[i], h[i], cudaIpcMemLazyEnablePeerAccess);
       if (e != cudaSuccess) {
         for (int j = 0; j < i; ++j) cudaIpcCloseMemHandle(p[j]);
@@ -1781,6 +1786,7 @@ int cake_tp_peer_open(cake_model* m, const void* all, int nranks) {
     m->peer_xn[r] = static_cast<bf16*>(p[1]);
     m->peer_h[r] = static_cast<float*>(p[2]);
     m->peer_flags[r] = static_cast<unsigned long long*>(p[3]);
+    m->peer_logits[r] = static_cast<float*>(p[4]);
   }
   m->peer_tp = true;
   return CAKE_OK;
@@ -1927,8 +1933,37 @@ int cake_final_logits(cake_model* m, long long T, const int32_t* d_last_token, i
                                                                        m->cfg.rms_eps, row, 1, nullptr);
     CKL();
   }
+  const int V = m->cfg.vocab;
+  if (m->peer_tp) {
+    // vocab-sharded LM head: rank r computes rows [r V / N, (r+1) V / N) and stores
+    // them into every rank's logits buffer; a flag barrier, then the assembled row is copied out
+    const int n = m->cfg.tp_size, r = m->cfg.tp_rank;
+    TpGemvArgs g{};
+    g.W = m->lm_head;
+    g.x = m->xn;
+    for (int q = 0; q < n; ++q) g.out[q] = m->peer_logits[q];
+    g.nranks = n;
+    g.n0 = static_cast<int>(static_cast<long long>(V) * r / n);
+    g.n1 = static_cast<int>(static_cast<long long>(V) * (r + 1) / n);
+    g.K = m->H;
+    {
+      const double rows = g.n1 - g.n0;
+      ProfScope ps(m, CAKE_K_LMHEAD, s, 2.0 * rows * m->H, 2.0 * rows * m->H);
+      const int grid = std::max(1, std::min((g.n1 - g.n0 + 7) / 8, num_sms() * 4));
+      tp_gemv_kernel<<<grid, 256, m->H * sizeof(float), s>>>(g);
+      CKL();
+    }
+    TpReduceArgs b{};
+    for (int q = 0; q < n; ++q) b.flags[q] = m->peer_flags[q];
+    b.rank = r;
+    b.nranks = n;
+    b.epoch = ++m->tp_epoch;
+    tp_barrier_kernel<<<1, 32, 0, s>>>(nullptr, b);
+    CKL();
+    CK(cudaMemcpyAsync(d_logits, m->tp_logits, static_cast<size_t>(V) * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    return CAKE_OK;
+  }
   {
-    const int V = m->cfg.vocab;
     ProfScope ps(m, CAKE_K_LMHEAD, s, 2.0 * V * m->H, 2.0 * V * m->H);
     const int threads = 256;
     const int grid = std::min((V + 7) / 8, num_sms() * 4);

@@ -171,4 +171,52 @@ __global__ void __launch_bounds__(kTpThreads) tp_reduce_kernel(const TpReduceArg
   if (blockIdx.x == 0 && threadIdx.x == 0) tp_wait_flags(mine, kTpFlagB, a.rank, a.nranks, a.epoch);
 }
 
+// Flag-only barrier of the TP group (same epochs and flag block as the
+// reductions): A = "my stores of this epoch are issued and fenced", then wait
+// for every peer's A. One thread.
+__global__ void tp_barrier_kernel(unsigned long long* const* flags_unused, const TpReduceArgs a) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int p = 0; p < a.nranks; ++p)
+    if (p != a.rank) st_release_sys(a.flags[p] + kTpFlagA + a.rank, a.epoch);
+  tp_wait_flags(a.flags[a.rank], kTpFlagA, a.rank, a.nranks, a.epoch);
+}
+
+// Vocab-sharded LM head of the first token: logits rows [n0, n1) of the
+// replicated weight, each stored into EVERY rank's logits buffer (one warp per
+// row, 16-B loads, x staged in shared memory as fp32; gemv_kernel's loop).
+struct TpGemvArgs {
+  const __nv_bfloat16* W;
+  const __nv_bfloat16* x;
+  float* out[kTpMaxRanks];
+  int nranks, n0, n1, K;
+};
+
+__global__ void tp_gemv_kernel(const TpGemvArgs a) {
+  extern __shared__ float xs_tp[];
+  for (int i = threadIdx.x; i < a.K; i += blockDim.x) xs_tp[i] = __bfloat162float(a.x[i]);
+  __syncthreads();
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int n = a.n0 + blockIdx.x * warps + (threadIdx.x >> 5); n < a.n1; n += gridDim.x * warps) {
+    const __nv_bfloat16* w = a.W + static_cast<size_t>(n) * a.K;
+    float acc = 0.f;
+#pragma unroll 4
+    for (int k = lane * 8; k < a.K; k += 256) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(w + k));
+      const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(p[e]);
+        acc += f.x * xs_tp[k + 2 * e] + f.y * xs_tp[k + 2 * e + 1];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, o);
+    if (lane == 0)
+      for (int r = 0; r < a.nranks; ++r) a.out[r][n] = acc;
+  }
+  __threadfence_system();  // the remote stores, before the barrier kernel that follows
+}
+
 }  // namespace cake_dev

@@ -226,7 +226,7 @@ def load_cuda():
     return lib
 
 
-TP_PEER_HANDLE_BYTES = 256  # include/cake_cuda.h CAKE_TP_PEER_HANDLE_BYTES
+TP_PEER_HANDLE_BYTES = 512  # include/cake_cuda.h CAKE_TP_PEER_HANDLE_BYTES
 
 
 def make_trace(points):
