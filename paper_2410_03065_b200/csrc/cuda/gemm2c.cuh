@@ -67,18 +67,17 @@ __device__ __forceinline__ void gemm2c_staged_resid(const GemmArgs& args, const 
                            pack_bf16(hv[2 * q + 1].x, hv[2 * q + 1].y), pack_bf16(hv[2 * q + 1].z, hv[2 * q + 1].w));
       *reinterpret_cast<uint4*>(sx + (c >> 1) * kHBox + row * 128 + ((j ^ sw) << 4)) = v;
     }
+    // store each box as soon as it is staged: box c's TMA store drains while boxes c+1.. are computed
+    fence_proxy_async();  // the generic-proxy smem writes, before the async-proxy (TMA) reads them
+    named_bar_sync(1, 128);
+    if (ep_tid == 0) {
+      const int n0 = n_blk * 128;
+      tma_store_2d(tm_h, sh + c * kHBox, n0 + c * 32, m0);
+      if ((c & 1) && args.xb_out != nullptr) tma_store_2d(tm_xb, sx + (c >> 1) * kHBox, n0 + (c >> 1) * 64, m0);
+    }
   }
   if (args.ss_out != nullptr && m < args.M) args.ss_out[static_cast<size_t>(n_blk) * args.ss_ld + m] = ss;
-  fence_proxy_async();  // the generic-proxy smem writes, before the async-proxy (TMA) reads them
-  named_bar_sync(1, 128);
   if (ep_tid == 0) {
-    const int n0 = n_blk * 128;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) tma_store_2d(tm_h, sh + c * kHBox, n0 + c * 32, m0);
-    if (args.xb_out != nullptr) {
-      tma_store_2d(tm_xb, sx, n0, m0);
-      tma_store_2d(tm_xb, sx + kHBox, n0 + 64, m0);
-    }
     bulk_commit();
     bulk_wait_read0();  // shared memory must outlive the reads
   }
