@@ -1958,7 +1958,7 @@ int cake_final_logits(cake_model* m, long long T, const int32_t* d_last_token, i
     b.rank = r;
     b.nranks = n;
     b.epoch = ++m->tp_epoch;
-    tp_barrier_kernel<<<1, 32, 0, s>>>(nullptr, b);
+    tp_barrier_kernel<<<1, 32, 0, s>>>(b);
     CKL();
     CK(cudaMemcpyAsync(d_logits, m->tp_logits, static_cast<size_t>(V) * sizeof(float), cudaMemcpyDeviceToDevice, s));
     return CAKE_OK;

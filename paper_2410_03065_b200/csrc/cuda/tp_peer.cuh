@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kTpThreads) tp_reduce_kernel(const TpReduceArg
 // Flag-only barrier of the TP group (same epochs and flag block as the
 // reductions): A = "my stores of this epoch are issued and fenced", then wait
 // for every peer's A. One thread.
-__global__ void tp_barrier_kernel(unsigned long long* const* flags_unused, const TpReduceArgs a) {
+__global__ void tp_barrier_kernel(const TpReduceArgs a) {
   if (threadIdx.x != 0) return;
   __threadfence_system();
   for (int p = 0; p < a.nranks; ++p)
