@@ -68,3 +68,34 @@ def test_bf16_variant_properties():
         # half a level + the bf16 rounding of the result (and of the fp16 header)
         bound = span / 255 / 2 + np.abs(v).max() * 2.0 ** -8 + span * 2.0 ** -10
         assert np.abs(y - v).max() <= bound
+
+
+def _dual_payloads(seed, count=12):
+    """Values exactly representable in BOTH fp16 and bf16 (8 significant bits, fp16 normal range), so the
+    reference's fp16 payload and the B200 tier's bf16 payload carry the same numbers."""
+    rng = np.random.default_rng(seed)
+    for _ in range(count):
+        n = int(rng.integers(1, 5000))
+        mant = rng.integers(128, 256, n)  # 8-bit significand
+        expo = rng.integers(-10, 8, n)
+        sign = rng.choice([-1.0, 1.0], n)
+        v = (sign * mant * np.exp2(expo - 7.0)).astype(np.float32)
+        yield v
+
+
+def test_bf16_variant_pinned_to_reference_lib(cake_ref):
+    """The bf16 tier encoding (the GPU's, bit-exact to kvcodec in tests/test_gpu_q8.py) equals the
+    reference library's fp16 encoding of the same values (codec.cpp:114-143: the levels and the fp16
+    (lo, hi) header depend only on the values); decoded values are the same fp32 result of
+    codec.cpp:158 rounded to bf16 instead of fp16, so they agree within the two roundings."""
+    for v in _dual_payloads(11):
+        f16 = v.astype(np.float16)
+        bf = kvcodec.f32_to_bf16_bits(v)
+        assert np.array_equal(f16.astype(np.float32), v) and np.array_equal(kvcodec.bf16_bits_to_f32(bf), v)
+        ref_enc = cake_ref.codec_encode("quant8", f16.tobytes())
+        enc = kvcodec.q8_encode(bf, "bf16")
+        assert enc == ref_enc
+        y16 = np.frombuffer(cake_ref.codec_decode("quant8", ref_enc, f16.nbytes), np.float16).astype(np.float64)
+        ybf = kvcodec.bf16_bits_to_f32(np.frombuffer(kvcodec.q8_decode(enc, bf.nbytes, "bf16"), np.uint16))
+        tol = np.abs(y16) * (2.0 ** -8 + 2.0 ** -11) + 2.0 ** -24
+        assert np.all(np.abs(ybf.astype(np.float64) - y16) <= tol)
