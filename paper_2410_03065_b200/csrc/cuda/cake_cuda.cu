@@ -22,6 +22,7 @@
 #ifdef CAKE_ATTN_VARIANTS  // experiment kernels (A/B only): make ATTN_VARIANTS=1
 #include "attention_fa4.cuh"
 #include "attention_dec.cuh"
+#include "attention_alt.cuh"
 #endif
 #include "cake_cuda.h"
 #include "elementwise.cuh"
@@ -830,7 +831,25 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
     // or every page for the q-only first-token pass (unaligned start, no KV write)
     fa.stable_pages = (chunk_start % kAttnPage) ? n_pages : static_cast<int>(chunk_start / kAttnPage);
 #ifdef CAKE_ATTN_VARIANTS
-    if (m->attn_impl == 4) {  // decoupled softmax groups (attention_dec.cuh)
+    if (m->attn_impl == 5) {  // softmax groups on alternate key blocks (attention_alt.cuh)
+      if (m->hd == 128) {
+        auto kern = attn_alt_kernel<128>;
+        static bool cfgd = false;
+        if (!cfgd) {
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FaltCfg<128>::kSmem));
+          cfgd = true;
+        }
+        CK(launch_chain(kern, grid, dim3(fa_threads<2>()), FaltCfg<128>::kSmem, s, 1, m->tm_q, m->tm_kv, fa));
+      } else {
+        auto kern = attn_alt_kernel<64>;
+        static bool cfgd = false;
+        if (!cfgd) {
+          CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FaltCfg<64>::kSmem));
+          cfgd = true;
+        }
+        CK(launch_chain(kern, grid, dim3(fa_threads<2>()), FaltCfg<64>::kSmem, s, 1, m->tm_q, m->tm_kv, fa));
+      }
+    } else if (m->attn_impl == 4) {  // decoupled softmax groups (attention_dec.cuh)
       if (m->hd == 128) {
         auto kern = attn_dec_kernel<128>;
         static bool cfgd = false;
@@ -1739,11 +1758,11 @@ CAKE_API int cake_debug_fa4_trace(void* dev_buf, int layer) {
 
 int cake_model_set_attention_impl(cake_model* m, int impl) {
 #ifndef CAKE_ATTN_VARIANTS
-  if (impl == 3 || impl == 4) return fail(CAKE_EINVAL, "attention impl %d: built without ATTN_VARIANTS=1", impl);
+  if (impl >= 3) return fail(CAKE_EINVAL, "attention impl %d: built without ATTN_VARIANTS=1", impl);
 #endif
-  if (impl < 0 || impl > 4)
+  if (impl < 0 || impl > 5)
     return fail(CAKE_EINVAL, "attention impl must be 0 (product dispatch), 1 (mma.sync), 2 (one-tile tcgen05), "
-                             "3 (two-tile tcgen05) or 4 (one-tile, decoupled softmax groups)");
+                             "3 (two-tile tcgen05), 4 (decoupled softmax groups) or 5 (groups on alternate blocks)");
   m->attn_impl = impl;
   return CAKE_OK;
 }

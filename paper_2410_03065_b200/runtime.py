@@ -224,7 +224,7 @@ class GpuRuntime:
         kernel for every chunk) or "mma_sync" (independent cross-check kernel)."""
         self.n.call("cake_gpu_set_attention_impl", self.h,
                     {"tcgen05": 0, "mma_sync": 1, "tcgen05_1tile": 2, "tcgen05_2tile": 3,
-                     "tcgen05_dec": 4}[impl])
+                     "tcgen05_dec": 4, "tcgen05_alt": 5}[impl])
 
     def set_profiling(self, kernels="all", stride: int = 1):
         """Bracket launches of the named kernel classes with CUDA events ("all", None, or a list);
