@@ -127,10 +127,11 @@ CAKE_API int cake_model_create(const cake_model_config* cfg, cake_model** out);
 CAKE_API int cake_model_create_shared(const cake_model_config* cfg, const cake_model* parent, cake_model** out);
 CAKE_API int cake_model_destroy(cake_model* m);
 CAKE_API int cake_model_get_info(const cake_model* m, cake_model_info* out);
-/* Attention kernel variant: 0 = product dispatch (the one-tile tcgen05/TMEM
- * flash attention kernel), 1 = mma.sync flash attention (independent
- * cross-check), 2 / 3 = the one-tile / two-tile tcgen05 kernel (tests), 4 = the
- * one-tile kernel with decoupled softmax groups (attention_dec.cuh). */
+/* Attention kernel variant: 0 = product dispatch (tcgen05/TMEM flash attention,
+ * softmax warpgroups on alternate key blocks, attention_alt.cuh), 1 = mma.sync
+ * flash attention (independent cross-check), 2 = the column-split one-tile
+ * tcgen05 kernel (attention_tc.cuh), 5 = the alternate-block kernel explicitly;
+ * 3 / 4 (two-tile, decoupled groups) need an ATTN_VARIANTS=1 build. */
 CAKE_API int cake_model_set_attention_impl(cake_model* m, int impl);
 /* NCCL plumbing for head-sharded TP (one process per GPU): rank 0 makes the
  * 128-byte id, the launcher broadcasts it, every rank inits its communicator. */

@@ -1,7 +1,9 @@
 // Prefix-causal attention, one 128-row Q tile per CTA, with the two softmax
-// warpgroups on ALTERNATE key blocks (impl 5, experiment build only).
+// warpgroups on ALTERNATE key blocks: the product kernel (cake_cuda.cu
+// attention(), impl 0; the column-split one-tile kernel of attention_tc.cuh
+// stays as impl 2).
 //
-// In the product kernel (attention_tc.cuh) both softmax warpgroups work on
+// In the one-tile kernel (attention_tc.cuh) both softmax warpgroups work on
 // the same 128-key block (column halves) and wait for the same S(j), so the
 // two warps of every SM sub-partition run the same phase at the same time and
 // the block's softmax (~1.5K cycles) bounds the block against the 1024-cycle
@@ -95,6 +97,40 @@ __global__ void __launch_bounds__(fa_threads<2>(), 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  // K/V blocks over stable pages (FaArgs::stable_pages: the prefix before the chunk, or the
+  // whole cache in the q-only first-token pass) are requested before the PDL wait
+  __shared__ int s_npre;
+  if (warp == 0 && lane == 0) {
+    int n_pre = 0;
+    if (tok0 < a.chunk_len) {
+      const long long planes0 = static_cast<long long>(a.n_layers) * 2 * a.n_kv_heads;
+      for (int j = 0; j < nb && j < Cfg::kKStages && j < Cfg::kVStages; ++j) {
+        const int lp0 = p_begin + 2 * j;
+        const int lp1 = (lp0 + 1 < p_end) ? lp0 + 1 : lp0;
+        if (lp1 >= a.stable_pages) break;
+        int32_t r[2][2];
+        for (int kv = 0; kv < 2; ++kv)
+          for (int q = 0; q < 2; ++q) {
+            const long long ph = a.block_table[q ? lp1 : lp0];
+            r[kv][q] = static_cast<int32_t>(
+                ((ph * planes0) + (static_cast<long long>(a.layer) * 2 + kv) * a.n_kv_heads + kvh) * 64);
+          }
+        mbar_arrive_expect_tx(&k_full[j], Cfg::kTileBytes);
+        mbar_arrive_expect_tx(&v_full[j], Cfg::kTileBytes);
+#pragma unroll
+        for (int h = 0; h < Cfg::kHalves; ++h) {
+          tma_load_2d(sK + j * Cfg::kTileBytes + h * Cfg::kHalfBytes, &tm_kv, &k_full[j], h * 64, r[0][0]);
+          tma_load_2d(sK + j * Cfg::kTileBytes + h * Cfg::kHalfBytes + Cfg::kPageHalfBytes, &tm_kv, &k_full[j],
+                      h * 64, r[0][1]);
+          tma_load_2d(sV + j * Cfg::kTileBytes + h * Cfg::kHalfBytes, &tm_kv, &v_full[j], h * 64, r[1][0]);
+          tma_load_2d(sV + j * Cfg::kTileBytes + h * Cfg::kHalfBytes + Cfg::kPageHalfBytes, &tm_kv, &v_full[j],
+                      h * 64, r[1][1]);
+        }
+        ++n_pre;
+      }
+    }
+    s_npre = n_pre;
+  }
   pdl_wait();
   pdl_trigger();
   if (threadIdx.x == 0) s_abort = a.abort_flag != nullptr ? *(volatile const int*)a.abort_flag : 0;
@@ -102,7 +138,13 @@ __global__ void __launch_bounds__(fa_threads<2>(), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int n_pre = s_npre;
   if (s_abort || tok0 >= a.chunk_len) {
+    if (warp == 0 && lane == 0)  // requested blocks must land before the shared memory goes away
+      for (int j = 0; j < n_pre; ++j) {
+        mbar_wait(&k_full[j], 0);
+        mbar_wait(&v_full[j], 0);
+      }
     if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tmem);
     return;
   }
@@ -116,7 +158,7 @@ __global__ void __launch_bounds__(fa_threads<2>(), 1)
     setmaxnreg_dec<56>();  // one instruction for the whole role warpgroup (.aligned)
     if (warp == 0) {
       if (lane == 0 && nb > 0) {
-        for (int j = 0; j < nb; ++j) {  // K blocks
+        for (int j = n_pre; j < nb; ++j) {  // K blocks
           const int s = j % Cfg::kKStages;
           mbar_wait(&k_empty[s], ((j / Cfg::kKStages) & 1) ^ 1u);
           const int lp0 = p_begin + 2 * j;
@@ -133,7 +175,7 @@ __global__ void __launch_bounds__(fa_threads<2>(), 1)
       }
     } else if (warp == 2) {
       if (lane == 0 && nb > 0) {
-        for (int j = 0; j < nb; ++j) {  // V blocks
+        for (int j = n_pre; j < nb; ++j) {  // V blocks
           const int s = j % Cfg::kVStages;
           mbar_wait(&v_empty[s], ((j / Cfg::kVStages) & 1) ^ 1u);
           const int lp0 = p_begin + 2 * j;

@@ -19,10 +19,10 @@
 
 #include "attention.cuh"
 #include "attention_tc.cuh"
+#include "attention_alt.cuh"
 #ifdef CAKE_ATTN_VARIANTS  // experiment kernels (A/B only): make ATTN_VARIANTS=1
 #include "attention_fa4.cuh"
 #include "attention_dec.cuh"
-#include "attention_alt.cuh"
 #endif
 #include "cake_cuda.h"
 #include "elementwise.cuh"
@@ -766,9 +766,9 @@ int attention_fa4(cake_model* m, long long chunk_start, int chunk_len, int layer
 
 int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, const int32_t* bt,
               const int32_t* abort_flag, cudaStream_t s) {
-  // Product dispatch (impl 0) is the one-tile kernel for every chunk: with
-  // FFMA2/FADD2 softmax it is faster than the two-tile kernel at every prefix
-  // measured (up to 32K, tools/attn_ab.py); impl 3 forces the two-tile kernel.
+  // Product dispatch (impl 0): one 128-row Q tile per CTA with the softmax warpgroups on
+  // alternate key blocks (attention_alt.cuh); impl 2 is the column-split one-tile kernel
+  // (attention_tc.cuh), impl 1 the mma.sync cross-check; 3 / 4 are experiment builds.
 #ifdef CAKE_ATTN_VARIANTS
   if (m->attn_impl == 3) return attention_fa4(m, chunk_start, chunk_len, layer, bt, abort_flag, s);
 #endif
@@ -830,8 +830,9 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
     // pages the predecessor cannot be writing: the prefix before a (page-aligned) prefill chunk,
     // or every page for the q-only first-token pass (unaligned start, no KV write)
     fa.stable_pages = (chunk_start % kAttnPage) ? n_pages : static_cast<int>(chunk_start / kAttnPage);
-#ifdef CAKE_ATTN_VARIANTS
-    if (m->attn_impl == 5) {  // softmax groups on alternate key blocks (attention_alt.cuh)
+    if (m->attn_impl == 0 || m->attn_impl == 5) {
+      // product: softmax warpgroups on alternate key blocks (attention_alt.cuh; 4.5% faster than the
+      // one-tile kernel at 32K, profiles/r02_attn_ab_micro.log)
       if (m->hd == 128) {
         auto kern = attn_alt_kernel<128>;
         static bool cfgd = false;
@@ -849,7 +850,9 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
         }
         CK(launch_chain(kern, grid, dim3(fa_threads<2>()), FaltCfg<64>::kSmem, s, 1, m->tm_q, m->tm_kv, fa));
       }
-    } else if (m->attn_impl == 4) {  // decoupled softmax groups (attention_dec.cuh)
+    } else
+#ifdef CAKE_ATTN_VARIANTS
+    if (m->attn_impl == 4) {  // decoupled softmax groups (attention_dec.cuh)
       if (m->hd == 128) {
         auto kern = attn_dec_kernel<128>;
         static bool cfgd = false;
@@ -1758,7 +1761,7 @@ CAKE_API int cake_debug_fa4_trace(void* dev_buf, int layer) {
 
 int cake_model_set_attention_impl(cake_model* m, int impl) {
 #ifndef CAKE_ATTN_VARIANTS
-  if (impl >= 3) return fail(CAKE_EINVAL, "attention impl %d: built without ATTN_VARIANTS=1", impl);
+  if (impl == 3 || impl == 4) return fail(CAKE_EINVAL, "attention impl %d: built without ATTN_VARIANTS=1", impl);
 #endif
   if (impl < 0 || impl > 5)
     return fail(CAKE_EINVAL, "attention impl must be 0 (product dispatch), 1 (mma.sync), 2 (one-tile tcgen05), "

@@ -220,8 +220,9 @@ class GpuRuntime:
         return out.raw
 
     def set_attention_impl(self, impl: str):
-        """"tcgen05" (product dispatch), "tcgen05_1tile" / "tcgen05_2tile" (one tcgen05
-        kernel for every chunk) or "mma_sync" (independent cross-check kernel)."""
+        """"tcgen05" (product dispatch: softmax warpgroups on alternate key blocks),
+        "tcgen05_1tile" (the column-split one-tile kernel), "mma_sync" (independent
+        cross-check kernel); "tcgen05_2tile" / "tcgen05_dec" need an ATTN_VARIANTS=1 build."""
         self.n.call("cake_gpu_set_attention_impl", self.h,
                     {"tcgen05": 0, "mma_sync": 1, "tcgen05_1tile": 2, "tcgen05_2tile": 3,
                      "tcgen05_dec": 4, "tcgen05_alt": 5}[impl])

@@ -210,6 +210,23 @@ def test_tcgen05_attention_matches_mma_sync_kernel(setup):
     assert rms_rel(lg_mma, setup["base_logits"]) <= TOL
 
 
+def test_one_tile_kernel_matches_product(setup):
+    """The column-split one-tile tcgen05 kernel (attention_tc.cuh, impl 2) against the product
+    kernel (softmax warpgroups on alternate key blocks, attention_alt.cuh): the whole computed
+    cache and the logits (same bf16 P; the per-group running max / the final merge differ)."""
+    rt, T, C = setup["rt"], setup["T"], setup["C"]
+    rt.set_attention_impl("tcgen05_1tile")
+    try:
+        prun(rt, setup["tier"], T, C, setup["seed"], mbps=1000, mode="compute_only")
+        one = [_chunk_kv(rt, s, C) for s in range(0, T, C)]
+        lg = rt.logits()
+    finally:
+        rt.set_attention_impl("tcgen05")
+    for i in range(len(one)):
+        assert rms_rel(one[i], _base(setup, i)) <= TOL
+    logits_ok(lg, setup["ref_logits"])
+
+
 def _base(setup, i):
     import llama_oracle
 
