@@ -168,6 +168,7 @@ struct GpuContext::Impl {
   const std::int32_t* final_bt = nullptr;
   std::vector<std::unique_ptr<Event>> ev_start, ev_near, ev_end, ev_io;
   std::unique_ptr<Event> ev_anchor, ev_copy_done, ev_final_start, ev_logits, ev_reset;  // created after set_device
+  std::unique_ptr<Event> ev_slice[2];  // the compute racer's layer slices (GpuPrefillBackend::launch)
   GpuRunInfo last;
   std::unique_ptr<TpCoordinator> tp;
   std::uint64_t run_counter = 0;
@@ -212,6 +213,8 @@ GpuContext::GpuContext(const GpuModelConfig& cfg, const GpuOptions& opt) : impl_
   g.ev_final_start = std::make_unique<Event>();
   g.ev_logits = std::make_unique<Event>();
   g.ev_reset = std::make_unique<Event>();
+  g.ev_slice[0] = std::make_unique<Event>();
+  g.ev_slice[1] = std::make_unique<Event>();
   check(opt.weights_from ? cake_model_create_shared(&mc, opt.weights_from->model(), &g.model)
                          : cake_model_create(&mc, &g.model),
         "model create");
@@ -561,6 +564,32 @@ class GpuPrefillBackend final : public PrefillBackend {
     const std::int32_t* tok = g.tokens.p + c.token_start;
     const std::int32_t* abort = g.abort_flags.p + c.index;
     check(cake_event_record(g.ev_start[c.index]->h, g.s_compute), "record");
+    if (contested && r_.tp == nullptr) {
+      // The racer is fed a few layers at a time, at most two slices ahead of the device: if the
+      // loader commits the chunk first, feeding stops and the little that is queued exits on the
+      // abort flag, so the first-token step is not stuck behind a whole lost chunk (a lost race
+      // used to cost ~1.8 ms of TTFT that way, tools/run_timeline.py). (TP: every rank must issue
+      // the same reductions, so a TP group enqueues the whole chunk.)
+      constexpr int kSlice = 4;
+      int k = 0;
+      for (int l0 = 0; l0 < L; l0 += kSlice, ++k) {
+        if (r_.commit[c.index].load() == kByIo) break;  // the loader landed it: stop feeding the device
+        const int l1 = std::min(L, l0 + kSlice);
+        check(cake_prefill_layers(g.model, tok, start, len, l0, l1, bt, abort, 0, g.s_compute), "prefill");
+        check(cake_event_record(g.ev_slice[k & 1]->h, g.s_compute), "record");
+        if (k > 0)  // keep at most two slices queued: wait for the previous one
+          while (cake_event_query(g.ev_slice[(k - 1) & 1]->h) != CAKE_OK) {
+            if (r_.commit[c.index].load() == kByIo) break;
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+          }
+      }
+      check(cake_event_record(g.ev_near[c.index]->h, g.s_compute), "record");  // (no next chunk paces on it)
+      check(cake_event_record(g.ev_end[c.index]->h, g.s_compute), "record");
+      std::lock_guard lk(mu_);
+      launched_.push_back(c.index);
+      predicted_end_.push_back(predicted);
+      return;
+    }
     check(cake_prefill_layers(g.model, tok, start, len, 0, split, bt, abort, 0, g.s_compute), "prefill");
     check(cake_event_record(g.ev_near[c.index]->h, g.s_compute), "record");
     if (split < L) check(cake_prefill_layers(g.model, tok, start, len, split, L, bt, abort, 0, g.s_compute), "prefill");
