@@ -57,6 +57,10 @@ def _worker(rank, world, port, shm, n, runs, q):
                 lib.call("cake_tp_end_compute", t)
                 th.join()
                 lib.call("cake_tp_end_io", t)
+                # a chunk the compute side committed: waiting for its shards returns at once
+                # (the loads were dropped) instead of waiting for shards that never land
+                lib.call("cake_tp_publish_decided", t, comp[0], 1)
+                lib.call("cake_tp_wait_all_landed", t, comp[0])
                 # the contested chunk of this run: compute's last entry raced (kRaceBit), io won it
                 lib.call("cake_tp_publish_decided", t, comp[-1], 2)
                 lib.call("cake_tp_publish_final", t, run % 2, 17 + run, comp[-1])
