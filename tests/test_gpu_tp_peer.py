@@ -42,18 +42,37 @@ def rms_rel(a, b):
     return float(np.sqrt(np.mean((a - b) ** 2)) / np.sqrt(np.mean(b ** 2)))
 
 
-def _rank(rank, world, port, shm, q):
+def _rank(rank, world, port, shm, q, reduce="peer", one_device=True):
+    import ctypes
+
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        from paper_2410_03065_b200 import native as N
         from paper_2410_03065_b200.runtime import GpuRuntime
 
-        rt = GpuRuntime(DIMS, max_tokens=T, max_chunk=CH, tp_rank=rank, tp_size=world, tp_shm=shm, device=0)
-        handles = [None] * world
-        dist.all_gather_object(handles, rt.tp_peer_handles())
-        rt.tp_peer_open(handles)
+        device = 0 if one_device else rank
+        kw = {}
+        if reduce == "nccl":  # the baseline reduction: the model's own NCCL communicator
+            cl = N.load_cuda()
+            cl.cake_cuda_set_device(device)
+            uid = (ctypes.c_uint8 * 128)()
+            if rank == 0:
+                assert cl.cake_nccl_unique_id(uid) == 0
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=0)
+            ctypes.memmove(uid, obj[0], 128)
+            comm = ctypes.c_void_p()
+            assert cl.cake_nccl_init(ctypes.byref(comm), uid, world, rank) == 0
+            kw["nccl_comm"] = comm.value
+        rt = GpuRuntime(DIMS, max_tokens=T, max_chunk=CH, tp_rank=rank, tp_size=world, tp_shm=shm, device=device,
+                        **kw)
+        if reduce == "peer":
+            handles = [None] * world
+            dist.all_gather_object(handles, rt.tp_peer_handles())
+            rt.tp_peer_open(handles)
         tier = rt.build_cache_tier(T, CH, SEED)
         out = {"rank": rank}
         runs = {"compute_only": dict(mode="compute_only", mbps=2000), "io_only": dict(mode="io_only", mbps=2000),
@@ -75,12 +94,18 @@ def _rank(rank, world, port, shm, q):
         dist.destroy_process_group()
 
 
-def test_tp2_peer_two_processes_one_gpu():
+@pytest.mark.parametrize("reduce,one_device", [("peer", True), ("peer", False), ("nccl", False)],
+                         ids=["peer-one-gpu", "peer-two-gpus", "nccl-two-gpus"])
+def test_tp2_two_processes(reduce, one_device):
+    """peer-one-gpu runs everywhere (both ranks on GPU 0); the two-GPU cases (real NVLink peer
+    mappings, and the NCCL baseline, which refuses two ranks on one device) need >= 2 GPUs."""
     import torch
     import torch.multiprocessing as mp
 
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
+    if not one_device and torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
     from paper_2410_03065_b200.runtime import GpuRuntime
 
     full = GpuRuntime(DIMS, max_tokens=T, max_chunk=CH)
@@ -92,9 +117,9 @@ def test_tp2_peer_two_processes_one_gpu():
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + (os.getpid() % 2000)
+    port = 29600 + (os.getpid() % 2000) * 4 + (0 if one_device else 1) + (2 if reduce == "nccl" else 0)
     shm = f"/cake_tp_peer_{uuid.uuid4().hex[:12]}"
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, shm, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, shm, q, reduce, one_device)) for r in range(2)]
     for p in procs:
         p.start()
     outs = sorted((q.get(timeout=600) for _ in procs), key=lambda o: o["rank"])
