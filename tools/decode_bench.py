@@ -26,6 +26,8 @@ model = lib.lib.cake_gpu_model(rt.h)
 cl = native.load_cuda()
 if os.environ.get("PREFETCH_KB") is not None:
     cl.cake_dec_set_prefetch(int(os.environ["PREFETCH_KB"]))
+if os.environ.get("ATTN_WAVES") is not None:
+    cl.cake_set_experiment(2, int(os.environ["ATTN_WAVES"]))  # CAKE_EXP_ATTN_MAX_WAVES
 if os.environ.get("CHAIN") is not None:
     cl.cake_set_experiment(4, int(os.environ["CHAIN"]))  # CAKE_EXP_DEC_CHAIN
 cl.cake_final_logits.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
