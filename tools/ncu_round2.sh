@@ -17,5 +17,5 @@ export T=16384 REPS=0
 # 4 launches per layer -> skip 20 chunks x 32 layers x 4 = 2560 for chunk 20, layer 0
 ncu --set full --clock-control none --import-source on -k regex:gemm2 -s 2560 -c 4 -o $OUT/${TAG}_gemm2 -f python tools/profile_step.py > $OUT/${TAG}_gemm2.log 2>&1
 # attention: chunk 28 (prefix 14K), layer 5
-ncu --set full --clock-control none --import-source on -k regex:attn_tc_kernel -s 901 -c 1 -o $OUT/${TAG}_attn2 -f python tools/profile_step.py > $OUT/${TAG}_attn2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"attn_(tc|alt)_kernel" -s 901 -c 1 -o $OUT/${TAG}_attn2 -f python tools/profile_step.py > $OUT/${TAG}_attn2.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:kv_permute -s 4 -c 1 -o $OUT/${TAG}_scatter -f python tools/profile_step.py > $OUT/${TAG}_scatter.log 2>&1
