@@ -372,7 +372,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& args, uint32_t tba
       const int half = hd >> 1;
       const int units_per_head = hd >> 6;
       const long long pos = args.pos0 + m;
-#pragma unroll 1
+#pragma unroll
       for (int k = 0; k < BLOCK_N / 64; ++k) {
         const int unit = n_blk * (BLOCK_N / 64) + k;
         const int head = unit / units_per_head;
