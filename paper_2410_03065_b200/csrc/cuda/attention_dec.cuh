@@ -1,7 +1,7 @@
 // Prefix-causal attention, one 128-row Q tile per CTA, with the two softmax
 // groups DECOUPLED (impl 4; cake_model_set_attention_impl).
 //
-// The product kernel (attention_tc.cuh) splits each 128-key block between two
+// The one-tile kernel (attention_tc.cuh) splits each 128-key block between two
 // softmax warpgroups by columns and exchanges the row max through shared
 // memory every block (a named barrier), so the two warps on each SM
 // sub-partition run the same phase at the same time: both on MUFU, then both on
