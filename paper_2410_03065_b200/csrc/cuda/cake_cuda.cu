@@ -1801,6 +1801,18 @@ int cake_tp_peer_open(cake_model* m, const void* all, int nranks) {
       cudaError_t e = cudaIpcOpenMemHandle(&p[i], h[i], cudaIpcMemLazyEnablePeerAccess);
       if (e != cudaSuccess) {
         for (int j = 0; j < i; ++j) cudaIpcCloseMemHandle(p[j]);
+        for (int q = 0; q < r; ++q)  // and every earlier peer's mappings: open is all or nothing
+          if (q != m->cfg.tp_rank)
+            for (void* b : {m->peer_part[q], static_cast<void*>(m->peer_xn[q]), static_cast<void*>(m->peer_h[q]),
+                            static_cast<void*>(m->peer_flags[q]), static_cast<void*>(m->peer_logits[q])})
+              if (b) cudaIpcCloseMemHandle(b);
+        for (int q = 0; q < kTpMaxRanks; ++q) {
+          m->peer_part[q] = nullptr;
+          m->peer_xn[q] = nullptr;
+          m->peer_h[q] = nullptr;
+          m->peer_flags[q] = nullptr;
+          m->peer_logits[q] = nullptr;
+        }
         return fail(CAKE_ECUDA + e, "tp peer: open rank %d buffer %d: %s", r, i, cudaGetErrorString(e));
       }
     }

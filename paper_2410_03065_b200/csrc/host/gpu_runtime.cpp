@@ -848,8 +848,11 @@ RunReport run_follower(GpuContext::Impl& g, TpCoordinator& tp, const RunPlan& pl
         aborted[i] = 1;
       }
   };
+  const Micros final_deadline = timer.now_us() + 300'000'000;  // a leader that died must not hang its followers
   while (!tp.final_published()) {
     maybe_abort();
+    if (timer.now_us() > final_deadline)
+      throw std::runtime_error("tp follower: the leader never published the first-token step's inputs");
     std::this_thread::sleep_for(std::chrono::microseconds(20));
   }
   maybe_abort();
