@@ -195,6 +195,13 @@ CAKE_API long long cake_kv_chunk_bytes(const cake_model* m, int chunk_len);
 CAKE_API int cake_kv_poison(cake_model* m, int byte, void* stream);
 /* staging bytes [byte_begin, byte_end) (16-B aligned) of a chunk starting at
  * token chunk_start -> paged pool through d_block_table. */
+/* Test entry: the model's attention kernel alone (the product dispatch, or the
+ * impl set by cake_model_set_attention_impl) for q rows d_q [chunk_len][local q
+ * heads][head_dim] bf16 at positions chunk_start.., over the paged KV of `layer`
+ * (keys <= each row's position); the output rows are copied to d_out (same
+ * shape). Lets tests compare the kernel with a plain fp32 attention. */
+CAKE_API int cake_attention_debug(cake_model* m, const void* d_q, long long chunk_start, int chunk_len, int layer,
+                                  const int32_t* d_block_table, void* d_out, void* stream);
 CAKE_API int cake_kv_scatter(cake_model* m, const void* d_staging, long long chunk_start, int chunk_len,
                     const int32_t* d_block_table, long long byte_begin, long long byte_end,
                     void* stream);

@@ -306,26 +306,28 @@ __global__ void __launch_bounds__(fa_threads<2>(), 1)
       for (int e = 8; e < kFaKeys; ++e) mc[e & 7] = fmaxf(mc[e & 7], __uint_as_float(su[e]));
       const float mx =
           fmaxf(fmaxf(fmaxf(mc[0], mc[1]), fmaxf(mc[2], mc[3])), fmaxf(fmaxf(mc[4], mc[5]), fmaxf(mc[6], mc[7]))) * sc;
-      if (mx > m + 8.0f) {  // (also true on the group's first block with a visible key)
-        if (m != -INFINITY) {
-          // O_g holds this group's blocks < j: wait for the PV of its previous block, then rescale
-          mbar_wait(&pv_done[g], (n - 1) & 1);
-          tc_fence_after();
-          const float f = ex2_approx(m - mx);
+      // tcgen05.ld/st are warp-collective (.sync.aligned): when any row of the warp moves its
+      // reference max the whole warp runs the rescale pass (factor 1 for the other rows)
+      const bool up = mx > m + 8.0f;  // (also true on the first block with a visible key)
+      const bool resc = up && m != -INFINITY;
+      if (__any_sync(0xffffffffu, resc)) {
+        // O_g holds this group's blocks < j: wait for the PV of its previous block, then rescale
+        mbar_wait(&pv_done[g], (n - 1) & 1);
+        tc_fence_after();
+        const float f = resc ? ex2_approx(m - mx) : 1.f;
 #pragma unroll
-          for (int c = 0; c < HD / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tO + c * 32, r);
-            tmem_ld_wait();
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tO + c * 32, r);
+          tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
-            tmem_st32(tO + c * 32, r);
-          }
-          tmem_st_wait();
-          l *= f;
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+          tmem_st32(tO + c * 32, r);
         }
-        m = mx;
+        tmem_st_wait();
+        l *= f;
       }
+      if (up) m = mx;
       const float nbase = (m == -INFINITY) ? 0.f : -m;
       const float2 sc2 = make_float2(sc, sc), nb2 = make_float2(nbase, nbase);
       float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};

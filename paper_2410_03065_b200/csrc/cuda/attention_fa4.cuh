@@ -322,29 +322,31 @@ __global__ void __launch_bounds__(kF4Threads, 1)
           mxv[c] = fmaxf(mxv[c], fmaxf(__uint_as_float(su[e + 2 * c]), __uint_as_float(su[e + 2 * c + 1])));
       const float mx = fmaxf(fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3])),
                              fmaxf(fmaxf(mxv[4], mxv[5]), fmaxf(mxv[6], mxv[7]))) * sc;  // scale > 0: max commutes
-      if (mx > m + 8.0f) {  // (also true on the first block with a visible key)
-        if (m != -INFINITY) {
-          // O_i holds blocks < j (PV_i(j-1) completed before S_i(j)): rescale it and l by 2^(m - mx)
-          const float f = ex2_approx(m - mx);
-          const float2 f2 = make_float2(f, f);
+      // tcgen05.ld/st are warp-collective (.sync.aligned): when any row of the warp moves its
+      // reference max the whole warp runs the rescale pass (factor 1 for the other rows)
+      const bool up = mx > m + 8.0f;  // (also true on the first block with a visible key)
+      const bool resc = up && m != -INFINITY;
+      if (__any_sync(0xffffffffu, resc)) {
+        // O_i holds blocks < j (PV_i(j-1) completed before S_i(j)): rescale it and l by 2^(m - mx)
+        const float f = resc ? ex2_approx(m - mx) : 1.f;
+        const float2 f2 = make_float2(f, f);
 #pragma unroll 1
-          for (int c = 0; c < HD / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tO + c * 32, r);
-            tmem_ld_wait();
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tO + c * 32, r);
+          tmem_ld_wait();
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-              float2 v = fmul2(make_float2(__uint_as_float(r[e]), __uint_as_float(r[e + 1])), f2);
-              r[e] = __float_as_uint(v.x);
-              r[e + 1] = __float_as_uint(v.y);
-            }
-            tmem_st32(tO + c * 32, r);
+          for (int e = 0; e < 32; e += 2) {
+            float2 v = fmul2(make_float2(__uint_as_float(r[e]), __uint_as_float(r[e + 1])), f2);
+            r[e] = __float_as_uint(v.x);
+            r[e + 1] = __float_as_uint(v.y);
           }
-          tmem_st_wait();
-          l *= f;
+          tmem_st32(tO + c * 32, r);
         }
-        m = mx;
+        tmem_st_wait();
+        l *= f;
       }
+      if (up) m = mx;
       if (tr && j < 64) trp[j * 8 + 3] = clock64();
       const float nb_ = (m == -INFINITY) ? 0.f : -m;
       const float2 nb2 = make_float2(nb_, nb_);

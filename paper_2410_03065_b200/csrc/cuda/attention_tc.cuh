@@ -419,27 +419,29 @@ __global__ void __launch_bounds__(fa_threads<NG>(), 1)
 #pragma unroll
       for (int h = 0; h < NG; ++h) mx = fmaxf(mx, xmax[s][h][row]);
       mx *= sc;  // scale > 0: max commutes
-      if (mx > m + 8.0f) {  // (also true on the first block with a visible key)
-        if (m != -INFINITY) {
-          // move the reference max: O (blocks < j, i.e. after PV(j-1)) and l scale by 2^(m - mx)
-          mbar_wait(pv_done, (j - 1) & 1);
-          tc_fence_after();
-          const float f = ex2_approx(m - mx);
-          const uint32_t tO = tmem + lane_off + Cfg::kColO + g * kOCols;
+      // tcgen05.ld/st are warp-collective (.sync.aligned): when any row of the warp moves its
+      // reference max the whole warp runs the rescale pass (factor 1 for the other rows)
+      const bool up = mx > m + 8.0f;  // (also true on the first block with a visible key)
+      const bool resc = up && m != -INFINITY;
+      if (__any_sync(0xffffffffu, resc)) {
+        // move the reference max: O (blocks < j, i.e. after PV(j-1)) and l scale by 2^(m - mx)
+        mbar_wait(pv_done, (j - 1) & 1);
+        tc_fence_after();
+        const float f = resc ? ex2_approx(m - mx) : 1.f;
+        const uint32_t tO = tmem + lane_off + Cfg::kColO + g * kOCols;
 #pragma unroll
-          for (int c = 0; c < kOCols / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tO + c * 32, r);
-            tmem_ld_wait();
+        for (int c = 0; c < kOCols / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tO + c * 32, r);
+          tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
-            tmem_st32(tO + c * 32, r);
-          }
-          tmem_st_wait();
-          l *= f;
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * f);
+          tmem_st32(tO + c * 32, r);
         }
-        m = mx;
+        tmem_st_wait();
+        l *= f;
       }
+      if (up) m = mx;
       const float nbase = (m == -INFINITY) ? 0.f : -m;
       const float2 sc2 = make_float2(sc, sc), nb2 = make_float2(nbase, nbase);
       float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};

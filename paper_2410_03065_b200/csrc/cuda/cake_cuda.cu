@@ -2011,6 +2011,21 @@ long long cake_kv_chunk_bytes(const cake_model* m, int chunk_len) {
   return 2LL * m->L * m->nkv * m->hd * 2 * chunk_len;
 }
 
+int cake_attention_debug(cake_model* m, const void* d_q, long long chunk_start, int chunk_len, int layer,
+                         const int32_t* d_block_table, void* d_out, void* stream) {
+  if (!m || !d_q || !d_out || !d_block_table) return fail(CAKE_EINVAL, "attention debug: null");
+  if (layer < 0 || layer >= m->L) return fail(CAKE_EINVAL, "attention debug: bad layer");
+  if (chunk_len < 1 || chunk_len > m->rows_cap) return fail(CAKE_EINVAL, "attention debug: chunk_len out of range");
+  if (chunk_start < 0 || chunk_start + chunk_len > static_cast<long long>(m->n_logical_pages) * m->cfg.page_tokens)
+    return fail(CAKE_EINVAL, "attention debug: beyond KV capacity");
+  cudaStream_t s = S(stream);
+  const size_t bytes = static_cast<size_t>(chunk_len) * m->nq * m->hd * sizeof(bf16);
+  CK(cudaMemcpyAsync(m->q, d_q, bytes, cudaMemcpyDeviceToDevice, s));
+  CKS(attention(m, chunk_start, chunk_len, layer, d_block_table, nullptr, s));
+  CK(cudaMemcpyAsync(d_out, m->attn, bytes, cudaMemcpyDeviceToDevice, s));
+  return CAKE_OK;
+}
+
 int cake_kv_poison(cake_model* m, int byte, void* stream) {
   if (!m) return fail(CAKE_EINVAL, "kv poison: null model");
   CK(cudaMemsetAsync(m->pool, byte & 0xFF, m->pool_bytes, S(stream)));

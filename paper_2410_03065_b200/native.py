@@ -221,6 +221,7 @@ def load_cuda():
     lib.cake_final_logits.argtypes = [vp, C.c_longlong, vp, C.c_int, C.c_int, vp, vp, vp]
     lib.cake_nccl_unique_id.argtypes = [vp]
     lib.cake_nccl_init.argtypes = [C.POINTER(vp), vp, C.c_int, C.c_int]
+    lib.cake_attention_debug.argtypes = [vp, vp, C.c_longlong, C.c_int, C.c_int, vp, vp, vp]
     lib.cake_tp_peer_handles.argtypes = [vp, vp, C.c_size_t]
     lib.cake_tp_peer_open.argtypes = [vp, vp, C.c_int]
     return lib

@@ -143,3 +143,73 @@ def test_kv_scatter_rejects_misaligned(cu, tiny_rt):
     model = tiny_rt.n.lib.cake_gpu_model(tiny_rt.h)
     assert cu.cake_kv_scatter(model, None, 32, 64, None, 0, 16, None) != 0  # not page aligned
     assert cu.cake_kv_scatter(model, None, 0, 64, None, 0, 10, None) != 0  # not 16-B aligned
+
+
+ATTN_MODELS = {
+    # name: dims (L, H, n_heads, n_kv, hd, ffn, vocab) — GQA 4:1 at hd 128 and 64, and 8:1
+    "gqa4_hd128": (1, 1024, 8, 2, 128, 1024, 32000),
+    "gqa4_hd64": (1, 512, 8, 2, 64, 1024, 32000),
+    "gqa8_hd128": (1, 2048, 16, 2, 128, 1024, 32000),
+}
+# (chunk_start, chunk_len): prefill chunks at several prefixes (odd and even 128-key block counts, a
+# ragged tail), and single-token rows at an unaligned position (split-KV + the combine)
+ATTN_CASES = [(0, 512), (512, 512), (1536, 512), (2048, 200), (0, 37), (3583, 1), (1000, 1)]
+
+
+@pytest.mark.parametrize("scores", ["flat", "growing"])
+@pytest.mark.parametrize("impl", ["tcgen05", "tcgen05_1tile", "mma_sync"])
+@pytest.mark.parametrize("name", list(ATTN_MODELS))
+def test_attention_kernel_matches_torch(cu, name, impl, scores):
+    """The attention kernels alone (cake_attention_debug) against a plain fp32 attention of the same
+    bf16 inputs: random K/V scattered into the paged pool through a permuted block table, random Q,
+    causal over the prefix. "growing" scales the keys up along the sequence, so rows move their
+    running max block after block at different times (the online-softmax rescale of O in TMEM runs
+    for some rows of a warp and not others: the case that once hung the tcgen05 kernels).
+    Tolerance: RMS-normalised error <= 2^-7 (bf16 P and output)."""
+    import torch
+
+    from paper_2410_03065_b200.runtime import GpuRuntime
+
+    dims = ATTN_MODELS[name]
+    L, H, nq, nkv, hd = dims[:5]
+    T = 4096
+    rt = GpuRuntime(dims, max_tokens=T, max_chunk=512)
+    rt.set_attention_impl(impl)
+    model = rt.n.lib.cake_gpu_model(rt.h)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    n_pages = T // 64
+    perm = torch.tensor(np.random.default_rng(1).permutation(n_pages).astype(np.int32), device="cuda")
+    # KV of every position in the tier's chunk layout [layer][K|V][kv head][token][hd], 512 tokens a chunk
+    kv = torch.randn(T, L, 2, nkv, hd, device="cuda", generator=g) * 2.0
+    if scores == "growing":
+        kv[:, :, 0] *= torch.linspace(0.5, 4.0, T, device="cuda")[:, None, None, None]
+    kv = kv.to(torch.bfloat16)
+    for s0 in range(0, T, 512):
+        staging = kv[s0:s0 + 512].permute(1, 2, 3, 0, 4).contiguous()
+        nbytes = cu.cake_kv_chunk_bytes(model, 512)
+        assert staging.numel() * 2 == nbytes
+        assert cu.cake_kv_scatter(model, staging.data_ptr(), s0, 512, perm.data_ptr(), 0, nbytes, _stream()) == 0, \
+            _err(cu)
+    G = nq // nkv
+    for start, length in ATTN_CASES:
+        q = (torch.randn(length, nq, hd, device="cuda", generator=g) * 2.0).to(torch.bfloat16)
+        out = torch.empty_like(q)
+        assert cu.cake_attention_debug(model, q.data_ptr(), start, length, 0, perm.data_ptr(), out.data_ptr(),
+                                       _stream()) == 0, _err(cu)
+        torch.cuda.synchronize()
+        end = start + length
+        k = kv[:end, 0, 0].float()  # [keys, nkv, hd]
+        v = kv[:end, 0, 1].float()
+        qf = q.float()
+        kh = k.repeat_interleave(G, dim=1)  # q head h reads kv head h // G
+        vh = v.repeat_interleave(G, dim=1)
+        scores = torch.einsum("thd,khd->htk", qf, kh) / hd ** 0.5
+        pos = torch.arange(start, end, device="cuda")[:, None]
+        keys = torch.arange(end, device="cuda")[None, :]
+        scores = scores.masked_fill((keys > pos)[None], float("-inf"))
+        ref = torch.einsum("htk,khd->thd", torch.softmax(scores, dim=-1), vh)
+        got = out.float()
+        assert torch.isfinite(got).all(), (name, impl, start, length)
+        err = float(torch.sqrt(torch.mean((got - ref) ** 2)) / torch.sqrt(torch.mean(ref ** 2)))
+        assert err <= 2.0 ** -7, (name, impl, start, length, err)
+    rt.close()
