@@ -262,7 +262,9 @@ CAKE_API int cake_gemm_set_schedule(int schedule);
  * GEMM_NOSPLIT 1 = no split-K for the few-tile pair GEMMs (0). */
 enum { CAKE_EXP_PDL = 0, CAKE_EXP_FUSED_NORM = 1, CAKE_EXP_ATTN_MAX_WAVES = 2, CAKE_EXP_GEMM_NOSPLIT = 3,
        CAKE_EXP_DEC_CHAIN = 4, /* 1: first-token projections on the persistent chain kernel, 0: per-projection GEMVs */
-       CAKE_EXP_COUNT = 5 };
+       CAKE_EXP_TP_OVERLAP = 5, /* 1: peer-TP prefill chunks run as two row micro-batches, each one's reductions
+                                   overlapping the other's projections; 0: one batch, reduce in line */
+       CAKE_EXP_COUNT = 6 };
 CAKE_API int cake_set_experiment(int knob, int value);
 /* First-token chain kernel: L2 prefetch per CTA ahead of each phase, in KB (A/B; default 128). */
 CAKE_API int cake_dec_set_prefetch(int kb);

@@ -79,7 +79,8 @@ cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 // the next kernel's CTAs become resident and run their prologue (barrier
 // init, TMEM alloc, descriptor prefetch) while the previous kernel drains.
 // A/B switches for measurements (cake_set_experiment); the defaults are the product.
-int g_exp[CAKE_EXP_COUNT] = {1 /*PDL*/, 1 /*FUSED_NORM*/, 1 /*ATTN_MAX_WAVES*/, 0 /*GEMM_NOSPLIT*/, 1 /*DEC_CHAIN*/};
+int g_exp[CAKE_EXP_COUNT] = {1 /*PDL*/, 1 /*FUSED_NORM*/, 1 /*ATTN_MAX_WAVES*/, 0 /*GEMM_NOSPLIT*/, 1 /*DEC_CHAIN*/,
+                              1 /*TP_OVERLAP*/};
 
 // cake_set_experiment(CAKE_EXP_PDL, 0) turns programmatic dependent launch off.
 bool pdl_enabled() { return g_exp[CAKE_EXP_PDL] != 0; }
@@ -599,6 +600,14 @@ struct cake_model {
   float* peer_logits[kTpMaxRanks]{};
   unsigned long long* peer_flags[kTpMaxRanks]{};
   unsigned long long tp_epoch = 0;
+  // micro-batch overlap of the peer reductions (prefill_overlap): the reduce stream, its
+  // events, and the activation maps rebased to the second micro-batch's first row
+  bool tp_defer = false;       // row_parallel: leave the partial for the caller to reduce
+  int attn_stable_cap = 1 << 30;  // attention: cap on FaArgs::stable_pages (second micro-batch)
+  cudaStream_t tp_rs = nullptr;
+  cudaEvent_t tp_ev[9]{};
+  int mb_r0 = -1;
+  CUtensorMap mb_xn[3], mb_attn[3], mb_act[3], mb_q;
   bool emulated_tp = false;  // test driver sums the ranks' partials itself (cake_prefill_group)
   unsigned profile_mask = 0;  // bit k: bracket launches of kernel class k with events
   int profile_stride = 1;     // bracket every n-th launch of a class (keeps the other PDL chains intact)
@@ -829,7 +838,8 @@ int attention(cake_model* m, long long chunk_start, int chunk_len, int layer, co
     fa.trace = (g_fa4_trace_layer == layer) ? g_fa4_trace : nullptr;
     // pages the predecessor cannot be writing: the prefix before a (page-aligned) prefill chunk,
     // or every page for the q-only first-token pass (unaligned start, no KV write)
-    fa.stable_pages = (chunk_start % kAttnPage) ? n_pages : static_cast<int>(chunk_start / kAttnPage);
+    fa.stable_pages = std::min(m->attn_stable_cap,
+                               (chunk_start % kAttnPage) ? n_pages : static_cast<int>(chunk_start / kAttnPage));
     if (m->attn_impl == 0 || m->attn_impl == 5) {
       // product: softmax warpgroups on alternate key blocks (attention_alt.cuh; 4.5% faster than the
       // one-tile kernel at 32K, profiles/r02_attn_ab_micro.log)
@@ -1215,6 +1225,7 @@ int row_parallel(cake_model* m, int kind, const CUtensorMap* ta, const CUtensorM
       ProfScope ps(m, kind, s, flops, bytes);
       CKS(gemm_dispatch(128, kEpiBf16, ta, tb, g, s));
     }
+    if (m->tp_defer) return CAKE_OK;  // prefill_overlap reduces it on the reduce stream
     return tp_reduce(m, M, false, next_gamma, s);
   }
   {
@@ -1293,6 +1304,143 @@ int layer_mlp_half(cake_model* m, int l, int M, const int32_t* d_abort, cudaStre
   }
   return row_parallel(m, CAKE_K_GEMM_D, m->a_act, lw.m_d, m->F, M, d_abort, s,
                       l + 1 < m->L ? m->layers[l + 1].ln1 : m->final_norm);
+}
+
+// ---- peer TP: two row micro-batches per chunk, reductions overlapped ----
+//
+// A chunk of M rows runs as micro-batches b = 0, 1 of Mb = M / 2 rows. Per layer the
+// compute stream s issues QKV_0 attn_0 O_0 | QKV_1 attn_1 O_1 | GU_0 D_0 | GU_1 D_1 and the
+// reduce stream r the four peer reductions R(O_0) R(O_1) R(D_0) R(D_1), each waiting on
+// its projection's event; each consumer waits on its reduction's event. So R(O_0) runs
+// under QKV_1 / attn_1 / O_1, R(O_1) under GU_0 / D_0, R(D_0) under GU_1 / D_1 and R(D_1)
+// under the next layer's QKV_0 / attn_0 / O_0. Every rank issues the reductions in the
+// same order on one stream (same epochs). Micro-batch 1 is micro-batch 0's suffix of the
+// same prompt, so its attention reads micro-batch 0's K/V (written by QKV_0 on s) — the
+// usual causal order. The two batches touch disjoint rows of every activation buffer, so
+// the reduction of one and the projections of the other never share bytes.
+
+// The model's row buffers seen from row r0 (the second micro-batch): pointers and TMA
+// maps rebased, restored on destruction. Launches capture their arguments when enqueued.
+struct RowView {
+  cake_model* m;
+  float *h, *tp_buf;
+  bf16 *xn, *q, *attn, *act;
+  void* part[kTpMaxRanks];
+  bf16* pxn[kTpMaxRanks];
+  CUtensorMap a_xn[3], a_attn[3], a_act[3], tm_q;
+  int cap;
+  RowView(cake_model* m_, int r0, int stable_cap) : m(m_) {
+    h = m->h, tp_buf = m->tp_buf, xn = m->xn, q = m->q, attn = m->attn, act = m->act, cap = m->attn_stable_cap;
+    for (int r = 0; r < kTpMaxRanks; ++r) part[r] = m->peer_part[r], pxn[r] = m->peer_xn[r];
+    std::memcpy(a_xn, m->a_xn, sizeof(a_xn));
+    std::memcpy(a_attn, m->a_attn, sizeof(a_attn));
+    std::memcpy(a_act, m->a_act, sizeof(a_act));
+    tm_q = m->tm_q;
+    if (r0 == 0) return;
+    const size_t H = m->H, QD = static_cast<size_t>(m->nq) * m->hd;
+    m->h += r0 * H;
+    m->tp_buf = reinterpret_cast<float*>(reinterpret_cast<bf16*>(m->tp_buf) + r0 * H);  // bf16 partial rows
+    m->xn += r0 * H;
+    m->q += r0 * QD;
+    m->attn += r0 * QD;
+    m->act += static_cast<size_t>(r0) * m->F;
+    for (int r = 0; r < m->cfg.tp_size; ++r) {
+      m->peer_part[r] = static_cast<bf16*>(m->peer_part[r]) + r0 * H;
+      m->peer_xn[r] += r0 * H;
+    }
+    std::memcpy(m->a_xn, m->mb_xn, sizeof(a_xn));
+    std::memcpy(m->a_attn, m->mb_attn, sizeof(a_attn));
+    std::memcpy(m->a_act, m->mb_act, sizeof(a_act));
+    m->tm_q = m->mb_q;
+    m->attn_stable_cap = stable_cap;
+  }
+  ~RowView() {
+    m->h = h, m->tp_buf = tp_buf, m->xn = xn, m->q = q, m->attn = attn, m->act = act, m->attn_stable_cap = cap;
+    for (int r = 0; r < kTpMaxRanks; ++r) m->peer_part[r] = part[r], m->peer_xn[r] = pxn[r];
+    std::memcpy(m->a_xn, a_xn, sizeof(a_xn));
+    std::memcpy(m->a_attn, a_attn, sizeof(a_attn));
+    std::memcpy(m->a_act, a_act, sizeof(a_act));
+    m->tm_q = tm_q;
+  }
+};
+
+bool overlap_ok(const cake_model* m, int M, bool no_kv) {
+  if (!m->peer_tp || m->emulated_tp || !g_exp[CAKE_EXP_TP_OVERLAP] || no_kv || M % 2) return false;
+  const int Mb = M / 2;
+  return Mb % kGemmBlockM == 0 && Mb % m->cfg.page_tokens == 0 && Mb % kAttnPage == 0 && Mb % m->cfg.tp_size == 0;
+}
+
+int overlap_setup(cake_model* m, int Mb) {
+  if (!m->tp_rs) {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&m->tp_rs, cudaStreamNonBlocking, hi));
+    for (auto& e : m->tp_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if (m->mb_r0 != Mb) {
+    const uint64_t R = m->rows_cap - Mb, H = m->H, QD = static_cast<uint64_t>(m->nq) * m->hd;
+    int st;
+    for (int i = 0; i < 3; ++i) {
+      if ((st = make_map(&m->mb_xn[i], m->xn + Mb * H, R, H, 128 >> i))) return st;
+      if ((st = make_map(&m->mb_attn[i], m->attn + Mb * QD, R, QD, 128 >> i))) return st;
+      if ((st = make_map(&m->mb_act[i], m->act + static_cast<uint64_t>(Mb) * m->F, R, m->F, 128 >> i))) return st;
+    }
+    const int G = m->nq / m->nkv;
+    if ((st = make_map_3d(&m->mb_q, m->q + Mb * QD, m->hd, m->nq, R, G, kFaRows / G))) return st;
+    m->mb_r0 = Mb;
+  }
+  return CAKE_OK;
+}
+
+int prefill_overlap(cake_model* m, long long chunk_start, int M, int lb, int le, const int32_t* bt,
+                    const int32_t* d_abort, cudaStream_t s) {
+  const int Mb = M / 2;
+  CKS(overlap_setup(m, Mb));
+  cudaStream_t r = m->tp_rs;
+  cudaEvent_t* ev = m->tp_ev;  // [0, 4): projections O_0 O_1 D_0 D_1 done; [4, 8): their reductions; 8: entry
+  const int kProj = 0, kRed = 4;
+  // the reduce stream starts after everything already on s (embed, the previous call's join)
+  CK(cudaEventRecord(ev[8], s));
+  CK(cudaStreamWaitEvent(r, ev[8], 0));
+  // micro-batch 1 must not request its chunk's K/V pages before the PDL wait: micro-batch 0
+  // writes them only three kernels earlier
+  const int cap1 = static_cast<int>(chunk_start / kAttnPage);
+  struct Defer {
+    cake_model* m;
+    explicit Defer(cake_model* m_) : m(m_) { m->tp_defer = true; }
+    ~Defer() { m->tp_defer = false; }
+  } defer(m);
+  auto reduce = [&](int b, int slot, const bf16* gamma) -> int {
+    CK(cudaEventRecord(ev[kProj + slot], s));
+    CK(cudaStreamWaitEvent(r, ev[kProj + slot], 0));
+    RowView v(m, b * Mb, cap1);
+    CKS(tp_reduce(m, Mb, false, gamma, r));
+    CK(cudaEventRecord(ev[kRed + slot], r));
+    return CAKE_OK;
+  };
+  for (int l = lb; l < le; ++l) {
+    LayerWeights& lw = m->layers[l];
+    const bf16* next_gamma = l + 1 < m->L ? m->layers[l + 1].ln1 : m->final_norm;
+    for (int b = 0; b < 2; ++b) {
+      if (l > lb) CK(cudaStreamWaitEvent(s, ev[kRed + 2 + b], 0));  // R(D_b) of layer l-1 pushed its xn rows
+      {
+        RowView v(m, b * Mb, cap1);
+        CKS(layer_attention_half(m, l, chunk_start + static_cast<long long>(b) * Mb, Mb, bt, d_abort, false, s));
+      }
+      CKS(reduce(b, b, lw.ln2));
+    }
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaStreamWaitEvent(s, ev[kRed + b], 0));  // R(O_b) pushed norm(h) rows into xn
+      {
+        RowView v(m, b * Mb, cap1);
+        CKS(layer_mlp_half(m, l, Mb, d_abort, s));
+      }
+      CKS(reduce(b, 2 + b, next_gamma));
+    }
+  }
+  // join: the caller's stream sees every reduction (the reduce stream is in order)
+  CK(cudaStreamWaitEvent(s, ev[kRed + 3], 0));
+  return CAKE_OK;
 }
 
 }  // namespace
@@ -1503,6 +1651,9 @@ int cake_model_destroy(cake_model* m) {
     cudaEventDestroy(p.b);
   }
   for (auto e : m->event_pool) cudaEventDestroy(e);
+  for (auto e : m->tp_ev)
+    if (e) cudaEventDestroy(e);
+  if (m->tp_rs) cudaStreamDestroy(m->tp_rs);
   delete m;
   return CAKE_OK;
 }
@@ -1899,6 +2050,7 @@ int cake_prefill_layers(cake_model* m, const int32_t* d_tokens, long long chunk_
     CKL();
   }
   const bool no_kv = (flags & CAKE_PREFILL_NO_KV_WRITE) != 0;
+  if (overlap_ok(m, M, no_kv)) return prefill_overlap(m, chunk_start, M, layer_begin, layer_end, d_block_table, d_abort, s);
   for (int l = layer_begin; l < layer_end; ++l) {
     CKS(layer_attention_half(m, l, chunk_start, M, d_block_table, d_abort, no_kv, s));
     CKS(layer_mlp_half(m, l, M, d_abort, s));

@@ -42,7 +42,7 @@ def rms_rel(a, b):
     return float(np.sqrt(np.mean((a - b) ** 2)) / np.sqrt(np.mean(b ** 2)))
 
 
-def _rank(rank, world, port, shm, q, reduce="peer", one_device=True):
+def _rank(rank, world, port, shm, q, reduce="peer", one_device=True, overlap=True):
     import ctypes
 
     import torch.distributed as dist
@@ -54,6 +54,8 @@ def _rank(rank, world, port, shm, q, reduce="peer", one_device=True):
         from paper_2410_03065_b200.runtime import GpuRuntime
 
         device = 0 if one_device else rank
+        if not overlap:  # one batch per chunk, every reduction in line (CAKE_EXP_TP_OVERLAP = 5)
+            N.load_cuda().cake_set_experiment(5, 0)
         kw = {}
         if reduce == "nccl":  # the baseline reduction: the model's own NCCL communicator
             cl = N.load_cuda()
@@ -85,8 +87,15 @@ def _rank(rank, world, port, shm, q, reduce="peer", one_device=True):
             rt.poison(0xFF)
             r = rt.run(tier, T, CH, SEED, **kw)
             out[name] = {"logits": rt.logits().copy(), "merge": r.merge_point, "raced": r.raced_chunk,
-                         "winner": r.race_winner, "recomputed": r.recomputed_last,
+                         "winner": r.race_winner, "recomputed": r.recomputed_last, "launches": r.kernel_launches,
                          "kv": [rt.read_chunk(s, CH) for s in range(0, T, CH)]}
+        if overlap and reduce == "peer":  # the same request with the in-line schedule, for comparison
+            cl = N.load_cuda()
+            cl.cake_set_experiment(5, 0)
+            rt.poison(0xFF)
+            r = rt.run(tier, T, CH, SEED, mode="compute_only", mbps=2000)
+            out["in_line"] = {"logits": rt.logits().copy(), "launches": r.kernel_launches}
+            cl.cake_set_experiment(5, 1)
         q.put(out)
         dist.barrier()
         rt.close()
@@ -94,11 +103,14 @@ def _rank(rank, world, port, shm, q, reduce="peer", one_device=True):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("reduce,one_device", [("peer", True), ("peer", False), ("nccl", False)],
-                         ids=["peer-one-gpu", "peer-two-gpus", "nccl-two-gpus"])
-def test_tp2_two_processes(reduce, one_device):
+@pytest.mark.parametrize("reduce,one_device,overlap",
+                         [("peer", True, True), ("peer", True, False), ("peer", False, True), ("nccl", False, True)],
+                         ids=["peer-one-gpu", "peer-one-gpu-in-line", "peer-two-gpus", "nccl-two-gpus"])
+def test_tp2_two_processes(reduce, one_device, overlap):
     """peer-one-gpu runs everywhere (both ranks on GPU 0); the two-GPU cases (real NVLink peer
-    mappings, and the NCCL baseline, which refuses two ranks on one device) need >= 2 GPUs."""
+    mappings, and the NCCL baseline, which refuses two ranks on one device) need >= 2 GPUs.
+    The peer cases run each chunk as two row micro-batches whose reductions overlap the other
+    batch's projections (CH = 256: two 128-row batches); "in-line" is the one-batch schedule."""
     import torch
     import torch.multiprocessing as mp
 
@@ -117,9 +129,10 @@ def test_tp2_two_processes(reduce, one_device):
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + (os.getpid() % 2000) * 4 + (0 if one_device else 1) + (2 if reduce == "nccl" else 0)
+    port = 29600 + (os.getpid() % 2000) * 8 + (0 if one_device else 1) + (2 if reduce == "nccl" else 0) + \
+        (0 if overlap else 4)
     shm = f"/cake_tp_peer_{uuid.uuid4().hex[:12]}"
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, shm, q, reduce, one_device)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, shm, q, reduce, one_device, overlap)) for r in range(2)]
     for p in procs:
         p.start()
     outs = sorted((q.get(timeout=600) for _ in procs), key=lambda o: o["rank"])
@@ -154,6 +167,14 @@ def test_tp2_two_processes(reduce, one_device):
             assert res["raced"] >= 0 and res["winner"] == spec["winner"], (r, case, res["raced"], res["winner"])
             want = o["io_only"]["logits"] if res["recomputed"] else c["logits"]
             assert np.array_equal(res["logits"], want), (r, case)
+        if "in_line" in o:
+            # the micro-batch schedule really ran (twice the projection / attention launches per layer; the
+            # leader's run report counts the run's launches) and agrees with the in-line schedule
+            if r == 0:
+                assert o["compute_only"]["launches"] > o["in_line"]["launches"], (o["compute_only"]["launches"],
+                                                                                  o["in_line"]["launches"])
+            assert rms_rel(o["in_line"]["logits"], want_logits) <= TOL
+            assert int(o["in_line"]["logits"].argmax()) == int(want_logits.argmax())
     # every rank ends with the same logits (replicated LM head over the same reduced rows)
     for name in ["cake"] + list(RACES):
         assert np.array_equal(outs[0][name]["logits"], outs[1][name]["logits"]), name
