@@ -32,6 +32,8 @@ if os.environ.get("CHAIN") is not None:
     cl.cake_set_experiment(4, int(os.environ["CHAIN"]))  # CAKE_EXP_DEC_CHAIN
 cl.cake_final_logits.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                  ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+if os.environ.get("IMPL"):  # e.g. tcgen05_alt: the 1-token attention on the tcgen05 kernel (before attention_q1)
+    rt.set_attention_impl(os.environ["IMPL"])
 r = rt.run(tier, T, 512, 42, mbps=256000, mode="io_only")
 print(f"run: final step {r.final_step_ms:.3f} ms (in situ)", flush=True)
 V = rt.vocab
