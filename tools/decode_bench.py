@@ -51,6 +51,14 @@ def step():
 for _ in range(3):
     step()
 torch.cuda.synchronize()
+import time  # noqa: E402
+enq = []
+for _ in range(5):  # host time to enqueue one step onto an idle stream (is the CPU ahead of the GPU?)
+    t0 = time.perf_counter()
+    step()
+    enq.append((time.perf_counter() - t0) * 1e3)
+    torch.cuda.synchronize()
+print(f"host enqueue of one step: {min(enq):.3f} ms (min of 5)", flush=True)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(REPS):
