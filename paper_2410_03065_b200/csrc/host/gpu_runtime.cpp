@@ -15,6 +15,7 @@
 #include <stdexcept>
 #include <thread>
 
+#include <cuda_runtime_api.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include "cake/gpu.hpp"
@@ -24,6 +25,18 @@
 namespace cake {
 
 namespace {
+
+// The CUDA current device is per host thread: the loader's reader / pacer threads and the TP
+// follower's io thread make CUDA calls too, so each binds the context's device before its first
+// call (a rank on device r > 0 would otherwise launch from device 0's context).
+void bind_device(int device) {
+  thread_local int bound = -1;
+  if (bound == device) return;
+  // cudaSetDevice alone: cake_cuda_set_device also drops the CUDA layer's cached SM count, which
+  // the compute thread may be reading
+  if (cudaSetDevice(device) != cudaSuccess) throw std::runtime_error("gpu: cannot bind the device to a worker thread");
+  bound = device;
+}
 
 // NVTX annotations (header-only nvtx3: free unless a tool such as nsys is
 // attached): the per-chunk, per-side timeline the reference keeps as its event
@@ -51,6 +64,7 @@ void pinned_release(void* p, void*) { cake_host_free(p); }
 // runs (a cudaHostAlloc of a 64-MiB chunk costs milliseconds; a run holds
 // only the chunk the reader fills and the ones the pacer is still copying).
 struct PinnedPool {
+  int device = -1;  // the context's device, bound by the (reader) thread that allocates
   std::mutex mu;
   std::multimap<std::size_t, void*> free_;  // size -> buffer
   std::unordered_map<void*, std::size_t> size_of;
@@ -68,6 +82,7 @@ struct PinnedPool {
         return p;
       }
     }
+    if (pool->device >= 0) bind_device(pool->device);
     void* p = pinned_alloc(n, nullptr);
     if (p) {
       std::lock_guard g(pool->mu);
@@ -189,6 +204,7 @@ GpuContext::GpuContext(const GpuModelConfig& cfg, const GpuOptions& opt) : impl_
   g.cfg = cfg;
   g.opt = opt;
   check(cake_cuda_set_device(opt.device), "set device");
+  g.landing.device = opt.device;
   if (opt.max_chunk % cfg.page_tokens) throw std::invalid_argument("gpu: max_chunk must be a multiple of page_tokens");
   cake_model_config mc{};
   mc.n_layers = cfg.n_layers;
@@ -544,6 +560,7 @@ class GpuPrefillBackend final : public PrefillBackend {
   GpuPrefillBackend(LiveRun& run, const CostModel& prior) : r_(run), prior_(prior) {}
 
   void pace() override {
+    bind_device(r_.g.opt.device);
     if (launched_.empty()) return;
     check(cake_event_sync(r_.g.ev_near[launched_.back()]->h), "pace");
     observe();
@@ -551,6 +568,7 @@ class GpuPrefillBackend final : public PrefillBackend {
 
   void launch(const ChunkSpec& c, bool contested) override {
     GpuContext::Impl& g = r_.g;
+    bind_device(g.opt.device);
     NvtxScope nv("compute chunk " + std::to_string(c.index) + (contested ? " (contested)" : ""));
     // followers enqueue the same chunk (reduction lockstep), the racer's entry through their spare pages
     if (r_.tp) r_.tp->publish_compute(c.index | (contested ? TpCoordinator::kRaceBit : 0u));
@@ -675,6 +693,7 @@ class GpuLoaderSink final : public ChunkSink {
 
   void begin_chunk(const FetchTask& t) override {
     GpuContext::Impl& g = r_.g;
+    bind_device(g.opt.device);
     if (range_) nvtxRangeEnd(range_);  // an abandoned chunk never reached end_chunk
     range_ = nvtxRangeStartA(("load chunk " + std::to_string(t.chunk.index) + (t.contested ? " (contested)" : "")).c_str());
     // every rank loads its shard of this chunk (the racer's entry into its spare pages)
@@ -686,12 +705,14 @@ class GpuLoaderSink final : public ChunkSink {
   }
 
   void deliver(const FetchTask& t, std::uint64_t offset, std::span<const std::byte> bytes) override {
+    bind_device(r_.g.opt.device);
     check(cake_h2d_async(buf_ + offset, bytes.data(), bytes.size(), r_.g.s_copy), "slice H2D");
     h2d_bytes_ += bytes.size();
   }
 
   void end_chunk(const FetchTask& t) override {
     GpuContext::Impl& g = r_.g;
+    bind_device(g.opt.device);
     if (q8_)
       check(cake_kv_scatter_q8(g.model, buf_, static_cast<long long>(t.chunk.token_start),
                                static_cast<int>(t.chunk.token_count), r_.table_for(t.chunk.index, kByIo), g.s_copy),
@@ -707,6 +728,7 @@ class GpuLoaderSink final : public ChunkSink {
   }
 
   Micros wait_chunk(const FetchTask& t) override {
+    bind_device(r_.g.opt.device);
     check(cake_event_sync(r_.g.ev_io[t.chunk.index]->h), "io wait");
     if (r_.tp) {  // resident only when every rank's KV-head shard landed
       r_.tp->shard_landed(t.chunk.index);
@@ -763,6 +785,7 @@ RunReport run_follower(GpuContext::Impl& g, TpCoordinator& tp, const RunPlan& pl
   std::exception_ptr io_error;
   std::thread io([&] {
     try {
+      bind_device(g.opt.device);
       const std::uint64_t quantum = std::max<std::uint64_t>(opt.throttle_quantum_bytes, 1);
       Micros budget = 0;
       for (std::uint32_t k = 0;; ++k) {
