@@ -54,6 +54,9 @@ CAKE_API int cake_cuda_last_error(char* buf, size_t len);
 CAKE_API int cake_cuda_version(int* runtime, int* driver);
 CAKE_API int cake_cuda_device_count(int* n);
 CAKE_API int cake_cuda_set_device(int device);
+/* Make `device` the calling thread's current device, only if it is not already (worker threads
+ * of the loader start on device 0; no cached state is dropped). */
+CAKE_API int cake_cuda_bind_thread(int device);
 CAKE_API int cake_cuda_sm_count(int device, int* n);
 CAKE_API int cake_cuda_device_sync(void);
 

@@ -1475,6 +1475,13 @@ int cake_cuda_set_device(int device) {
   return CAKE_OK;
 }
 
+int cake_cuda_bind_thread(int device) {
+  int cur = -1;
+  CK(cudaGetDevice(&cur));
+  if (cur != device) CK(cudaSetDevice(device));
+  return CAKE_OK;
+}
+
 int cake_cuda_sm_count(int device, int* n) {
   CK(cudaDeviceGetAttribute(n, cudaDevAttrMultiProcessorCount, device));
   return CAKE_OK;

@@ -15,7 +15,6 @@
 #include <stdexcept>
 #include <thread>
 
-#include <cuda_runtime_api.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include "cake/gpu.hpp"
@@ -26,15 +25,18 @@ namespace cake {
 
 namespace {
 
+void check(int st, const char* what);
+
 // The CUDA current device is per host thread: the loader's reader / pacer threads and the TP
 // follower's io thread make CUDA calls too, so each binds the context's device before its first
 // call (a rank on device r > 0 would otherwise launch from device 0's context).
 void bind_device(int device) {
   thread_local int bound = -1;
   if (bound == device) return;
-  // cudaSetDevice alone: cake_cuda_set_device also drops the CUDA layer's cached SM count, which
-  // the compute thread may be reading
-  if (cudaSetDevice(device) != cudaSuccess) throw std::runtime_error("gpu: cannot bind the device to a worker thread");
+  // through the CUDA layer (its runtime is the one whose current device matters; calling this
+  // library's own cudart would initialise a second runtime inside the run), and without
+  // cake_cuda_set_device's reset of the layer's cached SM count
+  check(cake_cuda_bind_thread(device), "bind device");
   bound = device;
 }
 
